@@ -1,0 +1,141 @@
+/*
+ * rkfac_b200.h -- C-ABI of the B200-native randomized K-FAC hot path.
+ *
+ * Drop-in boundary for the reference's operator API (/root/reference/proj/include/rkfac):
+ *
+ *   reference (C++, FP64, CPU)                                   this ABI (FP32 device buffers, sm_100a)
+ *   ------------------------------------------------------------ ------------------------------------------
+ *   void ea_update(EAKFactor&, const DenseMatrix& m)             rkfac_ea_update           (kfactor.hpp:33-41)
+ *   LowRankEig srevd(const DenseMatrix&, const SketchParams&,    rkfac_srevd               (rnla.hpp:90-105)
+ *                    RngState&)
+ *   LowRankEig rsvd_psd(const DenseMatrix&, const SketchParams&, rkfac_rsvd_psd            (rnla.hpp:81-85)
+ *                       RngState&)
+ *   DenseMatrix apply_lowrank_damped_inverse(const LowRankEig&,  rkfac_apply_lowrank_damped_inverse
+ *                    double, const DenseMatrix&, ApplySide)                                 (kfactor.hpp:134-161)
+ *   preconditioned_step's per-layer loop (optimizer.hpp:139-167) rkfac_plan_* (batched: every factor of every
+ *                                                                 layer in single launches)
+ *
+ * Conventions
+ *   - Every pointer argument named *_dev is a device pointer; matrices are row-major FP32 with an explicit
+ *     leading dimension (elements), exactly the reference's DenseMatrix layout (matrix.hpp:47-48).
+ *   - Calls are asynchronous on the context's CUDA stream (rkfac_set_stream), except where noted.
+ *   - No C++ exception crosses this ABI: every entry point returns an rkfac_status that mirrors the reference
+ *     exception types (errors.hpp:8-34); rkfac_last_error() gives the message.
+ *   - RngState& is passed as (seed, *counter).  Like sample_gaussian (rng.hpp:59-63) the counter advances by
+ *     2*d*w, so a caller that keeps a reference RngState stays bit-compatible with the CPU stream.
+ *   - There is no CPU fallback: without a usable sm_100 device every call returns RKFAC_CUDA_ERROR.
+ */
+#ifndef RKFAC_B200_H
+#define RKFAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RKFAC_OK = 0,
+    RKFAC_DIMENSION_MISMATCH = 1,  /* errors.hpp:8   DimensionMismatch  */
+    RKFAC_RANK_DEFICIENT = 2,      /* errors.hpp:12  RankDeficient      */
+    RKFAC_NO_CONVERGENCE = 3,      /* errors.hpp:16  NoConvergence      */
+    RKFAC_DAMPING_NONPOSITIVE = 4, /* errors.hpp:20  DampingNonpositive */
+    RKFAC_CUDA_ERROR = 5,
+    RKFAC_NCCL_ERROR = 6,
+    RKFAC_INVALID_ARGUMENT = 7
+} rkfac_status;
+
+typedef enum { RKFAC_RSVD = 0, RKFAC_SREVD = 1 } rkfac_method; /* DecompMethod, rnla.hpp:14 */
+typedef enum { RKFAC_LEFT = 0, RKFAC_RIGHT = 1 } rkfac_side;   /* ApplySide, kfactor.hpp:128 */
+
+typedef struct rkfac_context* rkfac_context_t;
+typedef struct rkfac_plan* rkfac_plan_t;
+
+/* ---- context ------------------------------------------------------------------------------------------ */
+int rkfac_create(rkfac_context_t* ctx, int device, void* cuda_stream);
+int rkfac_destroy(rkfac_context_t ctx);
+int rkfac_set_stream(rkfac_context_t ctx, void* cuda_stream);
+int rkfac_synchronize(rkfac_context_t ctx);
+const char* rkfac_last_error(rkfac_context_t ctx);
+const char* rkfac_status_string(int status);
+/* Kernels launched by this library since the context was created (the bench's gpu_launches count). */
+uint64_t rkfac_launch_count(rkfac_context_t ctx);
+
+/* ---- single-factor operators (the reference signatures) ---------------------------------------------- */
+
+/* rng.hpp:59-63 sample_gaussian: out (m x n row-major, FP32) = N(0,1) draws of RngState(seed) starting at
+ * *counter (Box-Muller, cos branch, FP64 math); *counter advances by 2*m*n.  Omega of srevd/rsvd_psd is this. */
+int rkfac_sample_gaussian(rkfac_context_t ctx, uint64_t seed, uint64_t* counter, int64_t m, int64_t n, float* out_dev,
+                          int64_t ld_out);
+
+/* kfactor.hpp:33-41: mbar (d x d) <- rho*mbar + (1-rho) * scale^2 * m m^T, m is d x n; mbar stays exactly
+ * symmetric (upper tiles computed, mirrored).  Rows of m != d -> RKFAC_DIMENSION_MISMATCH. */
+int rkfac_ea_update(rkfac_context_t ctx, float* mbar_dev, int64_t ld_mbar, int64_t d, const float* m_dev,
+                    int64_t ld_m, int64_t m_rows, int64_t n, double rho, double scale);
+
+/* rnla.hpp:90-105 srevd and rnla.hpp:81-85 rsvd_psd on a symmetric PSD x (d x d).
+ * Sketch clamping as rnla.hpp:35-43; *rank_out = clamped r.  u_dev: d x rank_out row-major (ld_u >= rank_out),
+ * dvals_dev: rank_out floats, descending.  Omega is drawn from (seed, *counter) exactly like the reference. */
+int rkfac_srevd(rkfac_context_t ctx, const float* x_dev, int64_t ld_x, int64_t d, int64_t r, int64_t p, int64_t q,
+                uint64_t seed, uint64_t* counter, float* u_dev, int64_t ld_u, float* dvals_dev, int64_t* rank_out);
+int rkfac_rsvd_psd(rkfac_context_t ctx, const float* x_dev, int64_t ld_x, int64_t d, int64_t r, int64_t p,
+                   int64_t q, uint64_t seed, uint64_t* counter, float* u_dev, int64_t ld_u, float* dvals_dev,
+                   int64_t* rank_out);
+
+/* kfactor.hpp:134-161.  u: dim x r (row-major, orthonormal columns), dvals: r.  LEFT needs rows == dim,
+ * RIGHT needs cols == dim.  lambda <= 0 -> RKFAC_DAMPING_NONPOSITIVE.  out may not alias v. */
+int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u_dev, int64_t ld_u,
+                                       const float* dvals_dev, int64_t dim, int64_t r, double lambda,
+                                       const float* v_dev, int64_t ld_v, int64_t rows, int64_t cols, int side,
+                                       float* out_dev, int64_t ld_out);
+
+/* ---- batched plan: every factor of every layer in single launches ------------------------------------ */
+
+typedef struct {
+    int64_t dim;          /* d */
+    int64_t rank;         /* r  (target_rank, before clamping) */
+    int64_t oversampling; /* p  (r_l)                            */
+    int64_t power_iters;  /* q  (n_pwr_it)                       */
+} rkfac_factor_desc;
+
+/* Creates a plan over nfactors factors decomposed with `method`.  The plan owns its workspaces; the caller
+ * owns factors, bases, eigenvalues, samples, gradients and outputs (bound below). */
+int rkfac_plan_create(rkfac_context_t ctx, const rkfac_factor_desc* descs, int nfactors, int method,
+                      rkfac_plan_t* plan);
+int rkfac_plan_destroy(rkfac_plan_t plan);
+/* Clamped rank of factor f (rnla.hpp:35-43). */
+int64_t rkfac_plan_rank(rkfac_plan_t plan, int f);
+
+/* factors[f]: d_f x d_f (ld = d_f).  bases_t[f]: Ut, rank_f x d_f (ld = d_f), i.e. U^T (the basis vectors
+ * contiguous).  dvals[f]: rank_f floats. */
+int rkfac_plan_bind_factors(rkfac_plan_t plan, float* const* factors_dev, float* const* bases_t_dev,
+                            float* const* dvals_dev);
+/* samples[f]: d_f x n_f (ld = n_f), the m argument of ea_update. */
+int rkfac_plan_bind_samples(rkfac_plan_t plan, const float* const* samples_dev, const int64_t* n);
+/* Layer l preconditions grads[l] (d_G x d_A, ld = d_A) with A-factor a_idx[l] and G-factor g_idx[l] into
+ * outs[l] (d_G x d_A); mids[l] is caller scratch of the same shape (RIGHT(A) result). */
+int rkfac_plan_bind_layers(rkfac_plan_t plan, int nlayers, const int* a_idx, const int* g_idx,
+                           const float* const* grads_dev, float* const* outs_dev, float* const* mids_dev);
+
+/* All factors: mbar <- rho*mbar + (1-rho)*scale^2 * m m^T (one launch). */
+int rkfac_plan_ea_update(rkfac_plan_t plan, double rho, double scale);
+/* All factors: rand-EVD with Omega_f from RngState(rng_root).substream(step, tag_f) (optimizer.hpp:189, 202),
+ * tag_f = f unless rkfac_plan_set_tags was called. */
+int rkfac_plan_decompose(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
+int rkfac_plan_set_tags(rkfac_plan_t plan, const uint64_t* tags);
+/* All layers: outs = LEFT_G(RIGHT_A(grads)) (optimizer.hpp:159-162). */
+int rkfac_plan_precondition(rkfac_plan_t plan, double lambda);
+/* EA (if samples bound) -> decompose -> precondition (if layers bound). */
+int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t rng_root, uint64_t step, double lambda);
+
+/* Per-stage device times (ms) of the last rkfac_plan_step / stage call, measured with CUDA events on the
+ * context stream: [0]=ea, [1]=decompose, [2]=precondition, [3]=decompose GEMM stage (XQ products only). */
+int rkfac_plan_stage_ms(rkfac_plan_t plan, float* ms4);
+/* Enable/disable per-stage event timing (adds events around stages; default off). */
+int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RKFAC_B200_H */

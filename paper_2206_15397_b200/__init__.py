@@ -1,0 +1,467 @@
+"""B200-native randomized K-FAC hot path (arXiv 2206.15397) behind the reference's operator API.
+
+Host side of the drop-in boundary.  The reference is C++ (``/root/reference/proj/include/rkfac``); its operator
+API is mirrored here name for name over the C-ABI in ``include/rkfac_b200.h`` (``librkfac_b200.so``, sm_100a):
+
+=========================================================  ==================================================
+reference (kfactor.hpp / rnla.hpp / optimizer.hpp)          this module
+=========================================================  ==================================================
+``EAKFactor``, ``ea_update(f, m)`` (kfactor.hpp:17-41)      ``EAKFactor``, ``ea_update(f, m)``
+``SketchParams``, ``RngState`` (rnla.hpp:26, rng.hpp:25)    ``SketchParams``, ``RngState``
+``srevd(x, p, rng)`` / ``rsvd_psd(x, p, rng)``              ``srevd`` / ``rsvd_psd`` -> ``LowRankEig``
+``apply_lowrank_damped_inverse(lr, lam, v, side)``          ``apply_lowrank_damped_inverse``
+``preconditioned_step`` layer loop (optimizer.hpp:139)      ``BatchedStep`` (all factors in single launches)
+exceptions (errors.hpp:8-34)                                ``DimensionMismatch``, ``DampingNonpositive``, ...
+=========================================================  ==================================================
+
+Tensors are CUDA ``torch.float32`` (PyTorch is plumbing here: device memory and streams).  There is no CPU
+fallback: if the library or an sm_100 device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Optional, Sequence
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librkfac_b200.so")
+
+# ---------------------------------------------------------------------------------------------- errors
+
+
+class RkfacError(RuntimeError):
+    status = -1
+
+
+class DimensionMismatch(RkfacError):  # errors.hpp:8
+    status = 1
+
+
+class RankDeficient(RkfacError):  # errors.hpp:12
+    status = 2
+
+
+class NoConvergence(RkfacError):  # errors.hpp:16
+    status = 3
+
+
+class DampingNonpositive(RkfacError):  # errors.hpp:20
+    status = 4
+
+
+class CudaError(RkfacError):
+    status = 5
+
+
+class NcclError(RkfacError):
+    status = 6
+
+
+class InvalidArgument(RkfacError):
+    status = 7
+
+
+_BY_STATUS = {c.status: c for c in (DimensionMismatch, RankDeficient, NoConvergence, DampingNonpositive, CudaError,
+                                    NcclError, InvalidArgument)}
+
+# ----------------------------------------------------------------------------------------- C-ABI binding
+
+_c_i64 = C.c_int64
+_c_u64 = C.c_uint64
+_vp = C.c_void_p
+
+
+class _FactorDesc(C.Structure):
+    _fields_ = [("dim", _c_i64), ("rank", _c_i64), ("oversampling", _c_i64), ("power_iters", _c_i64)]
+
+
+_lib = None
+
+#: every entry point of include/rkfac_b200.h, with (restype, argtypes)
+SIGNATURES = {
+    "rkfac_create": (C.c_int, [C.POINTER(_vp), C.c_int, _vp]),
+    "rkfac_destroy": (C.c_int, [_vp]),
+    "rkfac_set_stream": (C.c_int, [_vp, _vp]),
+    "rkfac_synchronize": (C.c_int, [_vp]),
+    "rkfac_last_error": (C.c_char_p, [_vp]),
+    "rkfac_status_string": (C.c_char_p, [C.c_int]),
+    "rkfac_launch_count": (_c_u64, [_vp]),
+    "rkfac_sample_gaussian": (C.c_int, [_vp, _c_u64, C.POINTER(_c_u64), _c_i64, _c_i64, _vp, _c_i64]),
+    "rkfac_ea_update": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_i64, C.c_double, C.c_double]),
+    "rkfac_srevd": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, C.POINTER(_c_u64), _vp,
+                              _c_i64, _vp, C.POINTER(_c_i64)]),
+    "rkfac_rsvd_psd": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, C.POINTER(_c_u64), _vp,
+                                 _c_i64, _vp, C.POINTER(_c_i64)]),
+    "rkfac_apply_lowrank_damped_inverse": (C.c_int, [_vp, _vp, _c_i64, _vp, _c_i64, _c_i64, C.c_double, _vp,
+                                                     _c_i64, _c_i64, _c_i64, C.c_int, _vp, _c_i64]),
+    "rkfac_plan_create": (C.c_int, [_vp, C.POINTER(_FactorDesc), C.c_int, C.c_int, C.POINTER(_vp)]),
+    "rkfac_plan_destroy": (C.c_int, [_vp]),
+    "rkfac_plan_rank": (_c_i64, [_vp, C.c_int]),
+    "rkfac_plan_bind_factors": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+    "rkfac_plan_bind_samples": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_c_i64)]),
+    "rkfac_plan_bind_layers": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(_vp),
+                                         C.POINTER(_vp), C.POINTER(_vp)]),
+    "rkfac_plan_set_tags": (C.c_int, [_vp, C.POINTER(_c_u64)]),
+    "rkfac_plan_ea_update": (C.c_int, [_vp, C.c_double, C.c_double]),
+    "rkfac_plan_decompose": (C.c_int, [_vp, _c_u64, _c_u64]),
+    "rkfac_plan_precondition": (C.c_int, [_vp, C.c_double]),
+    "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
+    "rkfac_plan_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "rkfac_plan_set_timing": (C.c_int, [_vp, C.c_int]),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads librkfac_b200.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: run `python -m paper_2206_15397_b200.build` (no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(status: int, ctx=None, what: str = ""):
+    if status != 0:
+        lib = load_library()
+        msg = lib.rkfac_last_error(ctx).decode() if lib.rkfac_last_error(ctx) else ""
+        raise _BY_STATUS.get(status, RkfacError)(f"{what}: {lib.rkfac_status_string(status).decode()}: {msg}")
+
+
+# --------------------------------------------------------------------------------------------- context
+
+_contexts: dict = {}
+
+
+def _torch():
+    import torch  # plumbing: device memory + streams
+
+    return torch
+
+
+class Context:
+    """One C-ABI context per (device); follows torch's current stream at each call."""
+
+    def __init__(self, device: int = 0):
+        torch = _torch()
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise CudaError("rkfac_b200 needs a CUDA device (sm_100); there is no CPU fallback")
+        self.device = device
+        h = _vp()
+        _check(lib.rkfac_create(C.byref(h), device, _vp(torch.cuda.current_stream(device).cuda_stream)), None,
+               "rkfac_create")
+        self.h = h
+        self.lib = lib
+
+    def sync_stream(self):
+        torch = _torch()
+        _check(self.lib.rkfac_set_stream(self.h, _vp(torch.cuda.current_stream(self.device).cuda_stream)), self.h,
+               "rkfac_set_stream")
+
+    def launches(self) -> int:
+        return int(self.lib.rkfac_launch_count(self.h))
+
+    def __del__(self):
+        try:
+            self.lib.rkfac_destroy(self.h)
+        except Exception:
+            pass
+
+
+def context(device: Optional[int] = None) -> Context:
+    torch = _torch()
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _contexts:
+        _contexts[dev] = Context(dev)
+    ctx = _contexts[dev]
+    ctx.sync_stream()
+    return ctx
+
+
+def _ptr(t) -> _vp:
+    return _vp(t.data_ptr())
+
+
+def _need_cuda_f32(t, name: str):
+    torch = _torch()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+        raise InvalidArgument(f"{name} must be a CUDA float32 tensor")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise InvalidArgument(f"{name} must be a row-major 2-D tensor")
+
+
+# ----------------------------------------------------------------------------------- reference types
+
+
+class DecompMethod(Enum):  # rnla.hpp:14
+    RSVD = 0
+    SREVD = 1
+    EXACT = 2
+
+
+class ApplySide(Enum):  # kfactor.hpp:128
+    LEFT = 0
+    RIGHT = 1
+
+
+@dataclass
+class SketchParams:  # rnla.hpp:26-30
+    target_rank: int = 1
+    oversampling: int = 0
+    power_iters: int = 0
+
+
+@dataclass
+class RngState:  # rng.hpp:25-56 (seed/counter only; draws happen on the device)
+    seed: int = 0
+    counter: int = 0
+
+    def substream(self, a: int, b: int = 0) -> "RngState":
+        return RngState(substream_seed(self.seed, a, b))
+
+
+def splitmix64(x: int) -> int:  # rng.hpp:13-18
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def substream_seed(seed: int, a: int, b: int = 0) -> int:  # rng.hpp:32-36
+    return splitmix64(seed ^ splitmix64(a ^ splitmix64(b)))
+
+
+@dataclass
+class LowRankEig:  # rnla.hpp:17-24: u (d x r, orthonormal columns), d (r, descending)
+    u: object
+    d: object
+    method: DecompMethod = DecompMethod.RSVD
+
+    def rank(self) -> int:
+        return int(self.d.shape[0])
+
+    def dim(self) -> int:
+        return int(self.u.shape[0])
+
+
+@dataclass
+class EAKFactor:  # kfactor.hpp:17-31
+    mbar: object
+    rho: float = 0.95
+    steps: int = 0
+
+    @staticmethod
+    def create(dim: int, rho: float, zero_init: bool = False, device=None) -> "EAKFactor":
+        torch = _torch()
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        m = torch.zeros(dim, dim, device=dev) if zero_init else torch.eye(dim, device=dev)
+        return EAKFactor(m, rho)
+
+    def dim(self) -> int:
+        return int(self.mbar.shape[0])
+
+
+# ------------------------------------------------------------------------------------------ operators
+
+
+def sample_gaussian(rng: RngState, m: int, n: int, device=None):
+    """rng.hpp:59-63: m x n N(0,1) draws on the device (FP64 math, FP32 store); advances rng.counter."""
+    torch = _torch()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(m, n, device=dev, dtype=torch.float32)
+    ctx = context(out.device.index)
+    ctr = _c_u64(rng.counter)
+    _check(ctx.lib.rkfac_sample_gaussian(ctx.h, _c_u64(rng.seed), C.byref(ctr), m, n, _ptr(out), n), ctx.h,
+           "sample_gaussian")
+    rng.counter = int(ctr.value)
+    return out
+
+
+def ea_update(f: EAKFactor, m, scale: float = 1.0) -> None:
+    """kfactor.hpp:33-41: f.mbar <- rho f.mbar + (1-rho) scale^2 m m^T (in place on the device)."""
+    _need_cuda_f32(f.mbar, "mbar")
+    _need_cuda_f32(m, "m")
+    ctx = context(f.mbar.device.index)
+    _check(ctx.lib.rkfac_ea_update(ctx.h, _ptr(f.mbar), f.mbar.stride(0), f.dim(), _ptr(m), m.stride(0),
+                                   m.shape[0], m.shape[1], float(f.rho), float(scale)), ctx.h, "ea_update")
+    f.steps += 1
+
+
+def _decompose(fn_name: str, method: DecompMethod, x, params: SketchParams, rng: RngState) -> LowRankEig:
+    torch = _torch()
+    _need_cuda_f32(x, "x")
+    if x.shape[0] != x.shape[1]:
+        raise DimensionMismatch(f"{fn_name}: factor must be square")
+    d = x.shape[0]
+    r_cl = min(params.target_rank, d)
+    ctx = context(x.device.index)
+    u = torch.empty(d, max(1, r_cl), device=x.device, dtype=torch.float32)
+    dv = torch.empty(max(1, r_cl), device=x.device, dtype=torch.float32)
+    ctr = _c_u64(rng.counter)
+    rank = _c_i64(0)
+    fn = getattr(ctx.lib, fn_name)
+    _check(fn(ctx.h, _ptr(x), x.stride(0), d, params.target_rank, params.oversampling, params.power_iters,
+              _c_u64(rng.seed), C.byref(ctr), _ptr(u), u.stride(0), _ptr(dv), C.byref(rank)), ctx.h, fn_name)
+    rng.counter = int(ctr.value)
+    rr = int(rank.value)
+    return LowRankEig(u[:, :rr], dv[:rr], method)
+
+
+def srevd(x, params: SketchParams, rng: RngState) -> LowRankEig:
+    """rnla.hpp:90-105 (advances rng.counter by 2*d*w like sample_gaussian)."""
+    return _decompose("rkfac_srevd", DecompMethod.SREVD, x, params, rng)
+
+
+def rsvd_psd(x, params: SketchParams, rng: RngState) -> LowRankEig:
+    """rnla.hpp:81-85 (V-side basis)."""
+    return _decompose("rkfac_rsvd_psd", DecompMethod.RSVD, x, params, rng)
+
+
+def apply_lowrank_damped_inverse(lr: LowRankEig, lam: float, v, side: ApplySide):
+    """kfactor.hpp:134-161: LEFT (U D U^T + lam I)^{-1} V, RIGHT V (U D U^T + lam I)^{-1}."""
+    torch = _torch()
+    if lam <= 0.0:
+        raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+    _need_cuda_f32(v, "v")
+    u = lr.u.contiguous() if lr.u.stride(1) != 1 else lr.u
+    _need_cuda_f32(u, "u")
+    dv = lr.d.contiguous()
+    out = torch.empty_like(v, memory_format=torch.contiguous_format)
+    ctx = context(v.device.index)
+    _check(ctx.lib.rkfac_apply_lowrank_damped_inverse(ctx.h, _ptr(u), u.stride(0), _ptr(dv), lr.dim(), lr.rank(),
+                                                      float(lam), _ptr(v), v.stride(0), v.shape[0], v.shape[1],
+                                                      side.value, _ptr(out), out.stride(0)), ctx.h,
+           "apply_lowrank_damped_inverse")
+    return out
+
+
+# ------------------------------------------------------------------------------------- batched step
+
+
+@dataclass
+class LayerSpec:
+    """One K-FAC layer: A-factor dimension (d_in+1) and G-factor dimension (d_out) (network.hpp:51-80)."""
+
+    dim_a: int
+    dim_g: int
+
+
+@dataclass
+class BatchedStep:
+    """The batched preconditioned step (optimizer.hpp:139-167) for a fixed list of layers.
+
+    Factor ``2l`` is layer l's A-factor and ``2l+1`` its G-factor, so the decomposition seed of factor f is
+    ``RngState(root).substream(step, f)`` exactly as optimizer.hpp:189/202.  All tensors are allocated on the
+    device once; ``step()`` runs EA update -> rand-EVD of every factor -> preconditioning of every layer with one
+    launch per stage.
+    """
+
+    layers: Sequence[LayerSpec]
+    rank: int = 220
+    oversampling: int = 10
+    power_iters: int = 4
+    method: DecompMethod = DecompMethod.SREVD
+    n_samples: Sequence[int] = ()
+    device: int = 0
+    factor_indices: Optional[Sequence[int]] = None  # global factor tags (multi-GPU shards keep global seeds)
+    factors: list = field(default_factory=list, init=False)
+    bases_t: list = field(default_factory=list, init=False)
+    dvals: list = field(default_factory=list, init=False)
+    samples: list = field(default_factory=list, init=False)
+    grads: list = field(default_factory=list, init=False)
+    outs: list = field(default_factory=list, init=False)
+    mids: list = field(default_factory=list, init=False)
+
+    def __post_init__(self):
+        torch = _torch()
+        self.ctx = context(self.device)
+        lib = self.ctx.lib
+        dims = []
+        for L in self.layers:
+            dims += [L.dim_a, L.dim_g]
+        self.dims = dims
+        descs = (_FactorDesc * len(dims))(*[_FactorDesc(d, self.rank, self.oversampling, self.power_iters)
+                                           for d in dims])
+        h = _vp()
+        meth = 1 if self.method == DecompMethod.SREVD else 0
+        _check(lib.rkfac_plan_create(self.ctx.h, descs, len(dims), meth, C.byref(h)), self.ctx.h, "plan_create")
+        self.h = h
+        dev = torch.device("cuda", self.device)
+        self.ranks = [int(lib.rkfac_plan_rank(h, f)) for f in range(len(dims))]
+        for f, d in enumerate(dims):
+            self.factors.append(torch.zeros(d, d, device=dev))
+            self.bases_t.append(torch.zeros(self.ranks[f], d, device=dev))
+            self.dvals.append(torch.zeros(self.ranks[f], device=dev))
+        arr = lambda ts: (_vp * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
+        _check(lib.rkfac_plan_bind_factors(h, arr(self.factors), arr(self.bases_t), arr(self.dvals)), self.ctx.h,
+               "bind_factors")
+        if self.factor_indices is not None:
+            tags = (_c_u64 * len(dims))(*[int(t) for t in self.factor_indices])
+            _check(lib.rkfac_plan_set_tags(h, tags), self.ctx.h, "set_tags")
+        if self.n_samples:
+            ns = list(self.n_samples)
+            if len(ns) == 1:
+                ns = ns * len(dims)
+            for f, d in enumerate(dims):
+                self.samples.append(torch.zeros(d, ns[f], device=dev))
+            nn = (_c_i64 * len(dims))(*ns)
+            _check(lib.rkfac_plan_bind_samples(h, arr(self.samples), nn), self.ctx.h, "bind_samples")
+        nl = len(self.layers)
+        for L in self.layers:
+            self.grads.append(torch.zeros(L.dim_g, L.dim_a, device=dev))
+            self.outs.append(torch.zeros(L.dim_g, L.dim_a, device=dev))
+            self.mids.append(torch.zeros(L.dim_g, L.dim_a, device=dev))
+        a_idx = (C.c_int * nl)(*[2 * l for l in range(nl)])
+        g_idx = (C.c_int * nl)(*[2 * l + 1 for l in range(nl)])
+        _check(lib.rkfac_plan_bind_layers(h, nl, a_idx, g_idx, arr(self.grads), arr(self.outs), arr(self.mids)),
+               self.ctx.h, "bind_layers")
+
+    # stages
+    def ea_update(self, rho: float = 0.95, scale: float = 1.0):
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_ea_update(self.h, rho, scale), self.ctx.h, "plan_ea_update")
+
+    def decompose(self, rng_root: int, step: int):
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_decompose(self.h, _c_u64(rng_root), _c_u64(step)), self.ctx.h,
+               "plan_decompose")
+
+    def precondition(self, lam: float):
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_precondition(self.h, lam), self.ctx.h, "plan_precondition")
+
+    def step(self, rng_root: int, step: int, lam: float, rho: float = 0.95, scale: float = 1.0):
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_step(self.h, rho, scale, _c_u64(rng_root), _c_u64(step), lam), self.ctx.h,
+               "plan_step")
+
+    def set_timing(self, on: bool):
+        _check(self.ctx.lib.rkfac_plan_set_timing(self.h, 1 if on else 0), self.ctx.h, "set_timing")
+
+    def stage_ms(self):
+        out = (C.c_float * 4)()
+        _check(self.ctx.lib.rkfac_plan_stage_ms(self.h, out), self.ctx.h, "stage_ms")
+        return {"ea": out[0], "decompose": out[1], "precondition": out[2], "xq_gemm": out[3]}
+
+    def lowrank(self, f: int) -> LowRankEig:
+        meth = self.method if self.method != DecompMethod.EXACT else DecompMethod.SREVD
+        return LowRankEig(self.bases_t[f].t(), self.dvals[f], meth)
+
+    def __del__(self):
+        try:
+            self.ctx.lib.rkfac_plan_destroy(self.h)
+        except Exception:
+            pass

@@ -1,0 +1,135 @@
+// engine.cuh -- the batched rand-K-FAC step: every factor of every layer in single launches per stage.
+//
+//   EA update      (kfactor.hpp:33-41)   one grouped symmetric GEMM (upper tiles, mirrored) over all factors
+//   decomposition  (rnla.hpp:47-105)     Omega -> [X Q -> CholeskyQR] x (2q+1) -> core -> eig -> lift
+//   precondition   (kfactor.hpp:134-161, optimizer.hpp:159-162)  RIGHT(A) then LEFT(Gamma), 4 grouped GEMMs
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace rkfac_b200 {
+
+struct Context;
+
+struct FactorState {
+    int d = 0, r = 0, p = 0, q = 0, w = 0;  // clamped r, p; w = r + p
+    // bound (caller-owned)
+    float* X = nullptr;     // d x d
+    long long ldx = 0;
+    float* Ut = nullptr;    // r x d  (U^T)
+    long long ldu = 0;
+    float* dvals = nullptr; // r
+    const float* M = nullptr;  // d x n samples
+    long long n = 0;
+    uint64_t tag = 0;
+    // plan-owned workspace (carved from the arena)
+    float *B0 = nullptr, *B1 = nullptr;  // w x d each (ld = d)
+    double* G64 = nullptr;               // w x w (Gram, FP64)
+    float* G32 = nullptr;                // w x w (Gram, FP32)
+    double* Linv64 = nullptr;
+    float* Linv32 = nullptr;
+    int* flags = nullptr;                // w + 1
+    void* chol_scratch = nullptr;
+    float* core = nullptr;               // w x w
+    double *eig_scratch = nullptr, *refl = nullptr, *tau = nullptr, *dvec = nullptr, *evec = nullptr,
+           *evals = nullptr, *scr = nullptr, *z = nullptr;
+    unsigned char* piv = nullptr;
+    float* P = nullptr;                  // w x r
+    float* scale = nullptr;              // r
+    int* zflags = nullptr;               // r + 1
+    float* bracket = nullptr;            // r
+};
+
+struct LayerState {
+    int a = 0, g = 0;
+    const float* J = nullptr;  // dG x dA
+    float* out = nullptr;
+    float* mid = nullptr;
+    float *W1 = nullptr, *W2 = nullptr;  // plan-owned: dG x rA, rG x dA
+};
+
+class Plan {
+  public:
+    Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method);
+    ~Plan();
+
+    int nfactors() const { return (int)f_.size(); }
+    FactorState& factor(int i) { return f_[i]; }
+    int method() const { return method_; }
+
+    void bind_factors(float* const* X, const long long* ldx, float* const* Ut, const long long* ldu,
+                      float* const* dvals);
+    void bind_samples(const float* const* M, const int64_t* n);
+    void bind_layers(int nl, const int* a, const int* g, const float* const* J, float* const* out,
+                     float* const* mid);
+    void set_tags(const uint64_t* tags);
+    void set_explicit_seed(int f, uint64_t seed, uint64_t ctr0);
+
+    void ea_update(double rho, double scale);
+    // mode 1: seeds from substream(root, step, tag); mode 0: explicit seeds.
+    void decompose(int mode, uint64_t root, uint64_t step);
+    void precondition(double lambda);
+    void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
+
+    void set_timing(bool on) { timing_ = on; }
+    void stage_ms(float* out4) const;
+    bool has_samples() const { return samples_bound_; }
+    bool has_layers() const { return !layers_.empty(); }
+
+    // Algorithmic FLOPs of the decomposition GEMM stage ((2q+2) X-products), for roofline reporting.
+    double xq_flops() const;
+
+  private:
+    void build_decomp_stages();
+    void build_ea_stage(double rho, double scale);
+    void build_apply_stages(double lambda);
+    void orth(int src, int dst, bool fp64, cudaStream_t s);
+    void record(int idx, bool begin);
+
+    Context* ctx_;
+    int method_;
+    std::vector<FactorState> f_;
+    std::vector<LayerState> layers_;
+    DevBuf arena_, layer_arena_;
+    bool factors_bound_ = false, samples_bound_ = false;
+
+    // Stage objects (direction 0: B1 -> B0 / B0 -> B1 variants indexed [dir]).
+    std::unique_ptr<GemmBatch> xq_[2];        // X * (Q in B[dir^1]) -> Y in B[dir]
+    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2], gram32_[2], tri32_[2];  // orth of B[src] into B[dst]
+    std::unique_ptr<GemmBatch> core_[2];      // core from (Q in B[dir^1], Y in B[dir])
+    std::unique_ptr<GemmBatch> lift_[2];
+    std::unique_ptr<GemmBatch> ea_;
+    std::unique_ptr<GemmBatch> ap_[4];
+    DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
+    std::vector<OmegaDesc> omega_;
+    long long omega_total_ = 0;
+    int wmax_ = 0, rmax_ = 0;
+    double ea_rho_ = -1, ea_scale_ = -1, ap_lambda_ = -1;
+    int n_fp64_orth_ = 2;
+
+    bool timing_ = false;
+    cudaEvent_t ev_[8] = {};
+    std::vector<cudaEvent_t> xq_ev_;
+    float stage_ms_[4] = {0, 0, 0, 0};
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    uint64_t launches_at_create = 0;
+    // single-factor API plan cache
+    struct Cached {
+        int d, r, p, q, method;
+        std::unique_ptr<Plan> plan;
+        DevBuf ut, dv;
+    };
+    std::vector<Cached> cache;
+    DevBuf apply_ws;
+};
+
+}  // namespace rkfac_b200

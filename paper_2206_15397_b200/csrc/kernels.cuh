@@ -1,0 +1,91 @@
+// kernels.cuh -- per-factor descriptors and launchers of the non-GEMM kernels of the path.
+#pragma once
+
+#include "common.cuh"
+
+namespace rkfac_b200 {
+
+// Omega^T (w x d) for factor f: Omega_ij = gaussian(seed_f, ctr0_f + 2(i*w + j)), stored at out[j*ld + i]
+// (rng.hpp:59-63 fills row-major d x w; the transpose keeps the basis vectors contiguous).
+struct OmegaDesc {
+    int d, w;
+    long long ld;
+    float* out;
+    uint64_t tag;       // substream tag (factor index f in optimizer.hpp:189)
+    uint64_t seed;      // used when seeds are explicit
+    uint64_t ctr0;
+    long long offset;   // prefix of d*w over factors
+    int rowmajor;       // 1: out[i*ld + j] (rng.hpp layout, used by rkfac_sample_gaussian)
+};
+// mode 0: seed_f = desc.seed; mode 1: seed_f = substream(root, step, tag_f)
+void launch_omega(const OmegaDesc* d_descs, int nfactors, long long total, int mode, uint64_t root, uint64_t step,
+                  cudaStream_t s);
+
+struct CholDesc {
+    int w;
+    const void* G;   // w x w Gram (double or float)
+    void* Linv;      // w x w output (double or float), lower triangular
+    int* flags;      // w rank-deficiency flags
+    int* nflags;     // any flag
+    void* scratch;   // global fallback for the packed triangle + panel
+};
+size_t cholinv_smem_bytes(int wmax, bool fp64);
+void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, bool gram64, double tol,
+                    cudaStream_t s);
+
+struct CompleteDesc {
+    int w, d;
+    long long ldq;
+    float* Qt;
+    const int* flags;
+    const int* nflags;
+};
+void launch_complete(const CompleteDesc* d_descs, int nfactors, cudaStream_t s);
+
+struct EigDesc {
+    int n, r;            // core size (w) and number of eigenpairs wanted
+    const float* A;      // n x n core (FP32, symmetric up to rounding)
+    long long lda;
+    double* scratch;     // packed triangle fallback (n(n+1)/2)
+    double* refl;        // n x n reflectors
+    double* tau;         // n
+    double* dvec;        // n
+    double* evec;        // n
+    double* evals;       // r, descending
+    double* scr;         // 4*n*r inverse-iteration LU
+    unsigned char* piv;  // n*r
+    double* z;           // n x r tridiagonal eigenvectors
+    float* P;            // n x r eigenvectors of the core (FP32), ld = ldp
+    long long ldp;
+};
+size_t tridiag_smem_bytes(int nmax);
+void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaStream_t s);
+
+// Post-processing of the eigenvalues into the LowRankEig d-vector and the U-lift scales.
+//   srevd (rnla.hpp:102-104): dvals = max(0, lam[:r]); colscale = 1.
+//   rsvd_psd (eig.hpp:256-270): s = sqrt(max(0, mu)); zero modes (s <= tiny) get s = 0, scale 0 and a flag so
+//   the lifted column is completed to an orthonormal direction.
+struct PostDesc {
+    int r;
+    int method;          // RKFAC_SREVD / RKFAC_RSVD
+    const double* evals; // r
+    float* dvals;        // r (output)
+    float* scale;        // r (U-lift row scale)
+    int* flags;          // r zero-mode flags (rsvd)
+    int* nflags;
+};
+void launch_post(const PostDesc* d_descs, int nfactors, cudaStream_t s);
+
+// bracket_i = 1/(d_i + lambda) - 1/lambda = -d_i / (lambda (lambda + d_i)) (kfactor.hpp:140-142), FP64 math.
+struct BracketDesc {
+    int r;
+    const float* dvals;
+    float* out;
+};
+void launch_bracket(const BracketDesc* d_descs, int n, double lambda, cudaStream_t s);
+
+// Transposed copy: out[j*ldo + i] = in[i*ldi + j] for an rows x cols input (used by the single-factor API to
+// return U in the reference's d x r layout).
+void launch_transpose(const float* in, long long ldi, int rows, int cols, float* out, long long ldo, cudaStream_t s);
+
+}  // namespace rkfac_b200
