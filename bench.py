@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""bench.py -- the randomized K-FAC hot path (EA update -> rand-EVD of every factor -> damped low-rank
+preconditioning of every layer gradient) on the BASELINE config-3 workload: the VGG16_bn-shaped full step
+(32 factors, 16 layers, n=128, r=min(220,d), p=10, q=4, lambda=0.1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload vgg16|wide4096|wide16384]
+
+Our arm: one process per GPU (torchrun for N>1), layers LPT-sharded across ranks, one NCCL all-gather of the
+preconditioned gradients.  A step = one EA update of every factor + rand-EVD of every factor + preconditioning of
+every layer (+ the all-gather).  value = factors inverted per second of whole step (all ranks) = 32 / step time.
+Reference arm (--impl reference): the reference's own C++ CPU code (oracle/_ref, the unmodified headers) on the
+box's host cores, one factor per std::thread, on a bounded sample of the same workload, extrapolated to the
+whole step (see `cpu_baseline.sample`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "K-factor rand-EVD inversions/s and precond-step ms; % of TF32/HBM roofline"
+UNIT = "inversions/s"
+ROOT_SEED = 220615397  # synthetic factor statistics
+OMEGA_ROOT = 7
+GRAD_ROOT = 99
+
+VGG_A = [28, 577, 577, 1153, 1153, 2305, 2305, 2305, 4609, 4609, 4609, 4609, 4609, 513, 513, 513]
+VGG_G = [64, 64, 128, 128, 256, 256, 256, 512, 512, 512, 512, 512, 512, 512, 512, 10]
+
+WORKLOADS = {
+    # name: (layers [(dA, dG)], n, e, rank, p, q, lambda, ea warm-up steps)
+    "vgg16": ([(a, g) for a, g in zip(VGG_A, VGG_G)], 128, 1.0, 220, 10, 4, 0.1, 20),
+    "wide4096": ([(4096, 4096)], 128, 0.8, 220, 10, 4, 0.1, 50),
+    "wide16384": ([(16384, 16384)] * 4, 512, 1.2, 256, 16, 4, 0.05, 10),
+}
+
+
+def sketch_width(d, r, p):
+    return d if r > d else min(r + p, d)
+
+
+def work_model(layers, n, r, p, q):
+    """Algorithmic work per factor / layer."""
+    fac = []
+    for a, g in layers:
+        for d in (a, g):
+            w = sketch_width(d, r, p)
+            rr = min(r, d)
+            f_gemm = (2 * q + 2) * 2.0 * d * d * w + 2.0 * d * w * w + 2.0 * d * w * rr
+            f_orth = 6.0 * (2 * q + 1) * d * w * w
+            f_ea = 2.0 * n * d * d
+            b_ea = 8.0 * d * d + 4.0 * n * d
+            b_gemm = (2 * q + 2) * 4.0 * d * d
+            fac.append(dict(d=d, w=w, r=rr, f_gemm=f_gemm, f_orth=f_orth, f_ea=f_ea, b_ea=b_ea, b_gemm=b_gemm,
+                            f_xq_launch=2.0 * d * d * w))
+    lay = []
+    for i, (a, g) in enumerate(layers):
+        ra, rg = min(r, a), min(r, g)
+        wa, wg = sketch_width(a, r, p), sketch_width(g, r, p)
+        lay.append(dict(f_ap=4.0 * g * a * (ra + rg), b_ap=8.0 * g * a + 4.0 * (a * wa + g * wg)))
+    return fac, lay
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, device_index=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self.dev = device_index
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, nm in names.items():
+                    if mask & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s, threads=None):
+    """The reference's own code (oracle/_ref) on a bounded sample of the workload, on `threads` host cores.
+
+    The sample is the smallest layers (by decomposition cost) whose estimated makespan fits `budget_s`; the full
+    step time is extrapolated as kappa * LPT-makespan(full) with kappa = measured / modelled sample time, the
+    model being the algorithmic flops of SURVEY.md 8(d) at a rate calibrated on the sample itself."""
+    import numpy as np
+
+    import oracle
+
+    ref = oracle.best()
+    port = oracle.port()
+    cores = threads or os.cpu_count() or 1
+    fac, lay = work_model(layers, n, r, p, q)
+    cost_f = [f["f_gemm"] + f["f_orth"] + f["f_ea"] for f in fac]
+    cost_l = [cost_f[2 * i] + cost_f[2 * i + 1] + lay[i]["f_ap"] for i in range(len(layers))]
+    rate = 3.5e9  # flop/s per core, SURVEY.md 6 (refined after the run)
+
+    def lpt_makespan(costs, nthreads):
+        loads = [0.0] * max(1, nthreads)
+        for c in sorted(costs, reverse=True):
+            k = loads.index(min(loads))
+            loads[k] += c
+        return max(loads)
+
+    order = sorted(range(len(layers)), key=lambda i: cost_l[i])
+    chosen = []
+    for i in order:
+        trial = chosen + [i]
+        fcost = [cost_f[2 * j + w] for j in trial for w in (0, 1)]
+        if lpt_makespan(fcost, cores) / rate > budget_s and chosen:
+            break
+        chosen = trial
+    chosen.sort()
+    sub = [layers[i] for i in chosen]
+    # inputs in FP64 (zero-init EA from the same synthetic stream as the GPU run; untimed)
+    dims_a = [a for a, _ in sub]
+    dims_g = [g for _, g in sub]
+    factors, ms, ns = [], [], []
+    for j, li in enumerate(chosen):
+        for which, d in enumerate((layers[li][0], layers[li][1])):
+            f = 2 * li + which
+            x = np.zeros((d, d))
+            ms.append(port.synthetic_m(ROOT_SEED, 0, f, n, d, e))  # one EA update per factor in the timed step
+            factors.append(x)
+            ns.append(n)
+    grads, outs = [], []
+    for li in chosen:
+        a, g = layers[li]
+        jm, _ = port.sample_gaussian(port.substream(GRAD_ROOT, li, 0), 0, g, a)
+        grads.append(jm)
+        outs.append(np.zeros((g, a)))
+    # warm the factors with a few EA updates so the decomposition sees a non-trivial spectrum (untimed)
+    for k in range(1, 3):
+        for idx, (li, which) in enumerate([(li, w) for li in chosen for w in (0, 1)]):
+            d = layers[li][which]
+            factors[idx] = port.ea_update(factors[idx], port.synthetic_m(ROOT_SEED, k, 2 * li + which, n, d, e), 0.95)
+    nth = min(cores, 2 * len(chosen))
+    t0 = time.perf_counter()
+    if hasattr(ref, "step_threaded"):
+        ph = ref.step_threaded("srevd", nth, dims_a, dims_g, factors, ms, ns, 0.95, r, p, q, OMEGA_ROOT, 0, lam,
+                               grads, outs)
+        kind = "reference"
+    else:  # restatement, threaded via ctypes (GIL released)
+        kind = "port"
+        ph = None
+        fl = [(li, w) for li in chosen for w in (0, 1)]
+
+        def one(idx):
+            li, w = fl[idx]
+            xx = port.ea_update(factors[idx], ms[idx], 0.95)
+            return port.srevd(xx, r, p, q, port.substream(OMEGA_ROOT, 0, 2 * li + w), 0)
+
+        decs = oracle.parallel_map(one, range(len(fl)), nth)
+        for j in range(len(chosen)):
+            port.precondition(decs[2 * j][0], decs[2 * j][1], decs[2 * j + 1][0], decs[2 * j + 1][1], lam, grads[j])
+    t_sample = time.perf_counter() - t0
+    sample_cost = [cost_f[2 * j + w] for j in chosen for w in (0, 1)]
+    model_sample = lpt_makespan(sample_cost, nth) / rate
+    kappa = t_sample / model_sample
+    full_time = kappa * lpt_makespan(cost_f, cores) / rate
+    full_time = max(full_time, kappa * max(cost_f) / rate)
+    nf = len(fac)
+    desc = (f"reference srevd step (EA update + rand-EVD + RIGHT/LEFT apply) on layers {chosen} "
+            f"({2 * len(chosen)} of {nf} factors) with {nth} threads took {t_sample:.2f}s; whole-step time "
+            f"extrapolated as LPT makespan over {cores} cores of the per-factor algorithmic work "
+            f"(SURVEY.md 8(d)), calibrated on the sample: {full_time:.2f}s")
+    return {"value": nf / full_time, "unit": UNIT, "cores": nth, "kind": kind, "sample": desc,
+            "sample_seconds": t_sample, "extrapolated_step_s": full_time,
+            "phase_seconds": None if ph is None else [float(x) for x in ph]}
+
+
+def run_reference_arm(args, wl):
+    layers, n, e, r, p, q, lam, _ = wl
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference_sample(layers, n, e, r, p, q, lam, budget)
+        if i >= args.warmup:
+            vals.append(res["extrapolated_step_s"])
+    t = statistics.median(vals) if vals else res["extrapolated_step_s"]
+    nf = 2 * len(layers)
+    v = nf / t
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "factors": nf, "layers": len(layers), "rank": r,
+                       "oversampling": p, "power_iters": q, "lambda": lam, "n": n},
+            "cpu_baseline": {k: res[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------------------------------- our arm
+def run_ours(args, wl):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2206_15397_b200 as rk
+    from paper_2206_15397_b200.partition import GatherLayout, layer_cost, lpt_partition
+
+    layers, n, e, r, p, q, lam, warm_steps = wl
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    costs = [layer_cost(a, g, r, p) for a, g in layers]
+    parts = lpt_partition(costs, world)
+    mine = parts[rank]
+    sizes = [a * g for a, g in layers]
+    layout = GatherLayout.build(sizes, parts)
+    shapes = [(g, a) for a, g in layers]
+
+    specs = [rk.LayerSpec(layers[l][0], layers[l][1]) for l in mine]
+    tags = [2 * l + w for l in mine for w in (0, 1)]
+    step = rk.BatchedStep(specs, rank=r, oversampling=p, power_iters=q, method=rk.DecompMethod.SREVD,
+                          n_samples=[n], device=local, factor_indices=tags)
+    ctx = step.ctx
+    inv_sqrt_n = 1.0 / math.sqrt(n)
+
+    def fill_samples(k):
+        """M_f = X^T / sqrt(n), X = Z diag(s), Z = gaussian(substream(ROOT_SEED, k, f))."""
+        for i, f in enumerate(tags):
+            d = step.dims[i]
+            z = rk.sample_gaussian(rk.RngState(rk.substream_seed(ROOT_SEED, k, f)), n, d, device=dev)
+            s = torch.arange(1, d + 1, device=dev, dtype=torch.float64).pow(-e)
+            step.samples[i].copy_((z.double() * s[None, :] * inv_sqrt_n).t().float())
+
+    # untimed warm-up of the EA statistics (zero init)
+    for k in range(warm_steps):
+        fill_samples(k)
+        step.ea_update(0.95, 1.0)
+    fill_samples(warm_steps)  # the timed step's fresh statistics
+    for i, l in enumerate(mine):
+        a, g = layers[l]
+        j = rk.sample_gaussian(rk.RngState(rk.substream_seed(GRAD_ROOT, l, 0)), g, a, device=dev)
+        step.grads[i].copy_(j)
+    factors0 = [x.clone() for x in step.factors]  # every timed step starts from the same EA state
+    torch.cuda.synchronize()
+
+    send = torch.zeros(layout.chunk, dtype=torch.float32, device=dev)
+    recv = torch.empty(world * layout.chunk, dtype=torch.float32, device=dev)
+
+    def one_step():
+        step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
+        for i, l in enumerate(mine):
+            send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
+        if world > 1:
+            dist.all_gather_into_tensor(recv, send)
+        else:
+            recv.copy_(send)
+
+    def reset():
+        for x, x0 in zip(step.factors, factors0):
+            x.copy_(x0)
+
+    for _ in range(args.warmup):
+        reset()
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region: K steps (factor restore is outside the events) ----
+    stream = torch.cuda.current_stream(dev)
+    step.set_timing(True)
+    launches0 = ctx.launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            reset()
+            ev[i][0].record(stream)
+            one_step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_local = sum(step_ms) / len(step_ms)
+    timing = step.timing()
+    step.set_timing(False)
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    nf_total = 2 * len(layers)
+
+    # ---- e2e through the public API with host buffers (pinned H2D of inputs, D2H of results) ----
+    h_samples = [x.cpu().pin_memory() for x in step.samples]
+    h_grads = [x.cpu().pin_memory() for x in step.grads]
+    h_outs = [torch.empty_like(x, device="cpu").pin_memory() for x in step.outs]
+    h2d = sum(x.numel() * 4 for x in h_samples) + sum(x.numel() * 4 for x in h_grads)
+    d2h = sum(x.numel() * 4 for x in h_outs)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.warmup + args.steps):
+        reset()
+        if i >= args.warmup:
+            e2e_ev[i - args.warmup][0].record(stream)
+        for hs, ds in zip(h_samples, step.samples):
+            ds.copy_(hs, non_blocking=True)
+        for hg, dg in zip(h_grads, step.grads):
+            dg.copy_(hg, non_blocking=True)
+        one_step()
+        for ho, do in zip(h_outs, step.outs):
+            ho.copy_(do, non_blocking=True)
+        if i >= args.warmup:
+            e2e_ev[i - args.warmup][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_local = sum(a.elapsed_time(b) for a, b in e2e_ev) / args.steps
+    te = torch.tensor([e2e_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+
+    # ---- roofline of the dominant kernel (the grouped X*Q product) and per-stage fractions ----
+    fac, lay = work_model(layers, n, r, p, q)
+    mine_f = [fac[f] for f in tags]
+    peaks, basis = load_peaks()
+    xq_ms, xq_cnt = timing["xq_gemm"]
+    xq_avg = xq_ms / max(1, xq_cnt)
+    f_xq_launch = sum(f["f_xq_launch"] for f in mine_f)
+    achieved = f_xq_launch / (xq_avg * 1e-3) / 1e12
+    fp32_simt_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    ea_ms = timing["ea"][0] / max(1, timing["ea"][1])
+    ap_ms = timing["precondition"][0] / max(1, timing["precondition"][1])
+    ea_bytes = sum(f["b_ea"] for f in mine_f)
+    ap_bytes = sum(lay[l]["b_ap"] for l in mine)
+    stages = {k: (v[0] / max(1, v[1]) if k not in ("xq_gemm", "orth") else v[0] / max(1, args.steps))
+              for k, v in timing.items()}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s=args.cpu_budget)
+            except Exception as ex:  # noqa: BLE001
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
+        value = nf_total / (ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "factors": nf_total, "layers": len(layers), "rank": r,
+                       "oversampling": p, "power_iters": q, "lambda": lam, "n": n, "method": "srevd",
+                       "parallelism": f"layer-LPT x{world} + NCCL all-gather",
+                       "l2": "inputs (505 MB of factors) exceed the 126 MB L2; no flush",
+                       "value_def": "factors inverted per second of the whole step (EA + rand-EVD + precondition "
+                                    "+ all-gather) = factors / step time"},
+            "precond_step_ms": ms,
+            "stage_ms": stages,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": fp32_simt_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp32_simt_peak, "traffic": None,
+                         "kernel": "grouped X*Q product (all factors, one launch), FP32 SIMT",
+                         "peak_basis": f"FP32 SIMT nominal 148 SM x 128 FMA x 2 x {peaks.get('sm_max_mhz', 1965)} "
+                                       f"MHz (the arithmetic this kernel issues); TF32 tensor = "
+                                       f"{peaks['bf16_tflops'] / 2:.0f} ({basis} bf16 / 2)",
+                         "frac_of_tf32": achieved / (peaks["bf16_tflops"] / 2.0)},
+            "ea_hbm": {"achieved_gbs": ea_bytes / (ea_ms * 1e-3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
+                       "frac": ea_bytes / (ea_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "apply_hbm": {"achieved_gbs": ap_bytes / (ap_ms * 1e-3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
+                          "frac": ap_bytes / (ap_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "e2e": {"value": nf_total / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches // max(1, args.steps),
+            "gpu_launches_total": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -129,11 +129,12 @@ int rkfac_plan_precondition(rkfac_plan_t plan, double lambda);
 /* EA (if samples bound) -> decompose -> precondition (if layers bound). */
 int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t rng_root, uint64_t step, double lambda);
 
-/* Per-stage device times (ms) of the last rkfac_plan_step / stage call, measured with CUDA events on the
- * context stream: [0]=ea, [1]=decompose, [2]=precondition, [3]=decompose GEMM stage (XQ products only). */
-int rkfac_plan_stage_ms(rkfac_plan_t plan, float* ms4);
-/* Enable/disable per-stage event timing (adds events around stages; default off). */
+/* Stage timing with CUDA events on the context stream, recorded inside the calls and harvested after the caller
+ * synchronises (no host sync inside a step).  set_timing(1) enables and resets.  rkfac_plan_timing fills 7 sums (ms)
+ * and 7 counts indexed: 0 EA update, 1 decomposition, 2 preconditioning, 3 X*Q products (the GEMM stage),
+ * 4 orthonormalisations, 5 core + eigensolve + lift, 6 whole step. */
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
+int rkfac_plan_timing(rkfac_plan_t plan, float* sums_ms7, int* counts7);
 
 #ifdef __cplusplus
 }

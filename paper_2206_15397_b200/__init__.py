@@ -108,7 +108,7 @@ SIGNATURES = {
     "rkfac_plan_decompose": (C.c_int, [_vp, _c_u64, _c_u64]),
     "rkfac_plan_precondition": (C.c_int, [_vp, C.c_double]),
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
-    "rkfac_plan_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "rkfac_plan_set_timing": (C.c_int, [_vp, C.c_int]),
 }
 
@@ -451,10 +451,14 @@ class BatchedStep:
     def set_timing(self, on: bool):
         _check(self.ctx.lib.rkfac_plan_set_timing(self.h, 1 if on else 0), self.ctx.h, "set_timing")
 
-    def stage_ms(self):
-        out = (C.c_float * 4)()
-        _check(self.ctx.lib.rkfac_plan_stage_ms(self.h, out), self.ctx.h, "stage_ms")
-        return {"ea": out[0], "decompose": out[1], "precondition": out[2], "xq_gemm": out[3]}
+    TIMING_KINDS = ("ea", "decompose", "precondition", "xq_gemm", "orth", "eig", "step")
+
+    def timing(self):
+        """{stage: (total ms, count)} since set_timing(True); call after torch.cuda.synchronize()."""
+        sums = (C.c_float * 7)()
+        cnts = (C.c_int * 7)()
+        _check(self.ctx.lib.rkfac_plan_timing(self.h, sums, cnts), self.ctx.h, "timing")
+        return {k: (float(sums[i]), int(cnts[i])) for i, k in enumerate(self.TIMING_KINDS)}
 
     def lowrank(self, f: int) -> LowRankEig:
         meth = self.method if self.method != DecompMethod.EXACT else DecompMethod.SREVD

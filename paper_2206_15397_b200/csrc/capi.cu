@@ -290,8 +290,8 @@ int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t root, 
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->step(rho, scale, root, step, lambda); });
 }
 
-int rkfac_plan_stage_ms(rkfac_plan_t plan, float* ms4) {
-    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->stage_ms(ms4); });
+int rkfac_plan_timing(rkfac_plan_t plan, float* sums_ms, int* counts) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->timing_report(sums_ms, counts); });
 }
 
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled) {

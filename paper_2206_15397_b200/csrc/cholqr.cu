@@ -36,7 +36,6 @@ __global__ void __launch_bounds__(1024) cholinv_kernel(const CholDesc* __restric
     const int tid = threadIdx.x, nthr = blockDim.x;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* L = use_smem ? reinterpret_cast<T*>(smem_raw) : static_cast<T*>(cd.scratch);
-    T* P = L + (long long)n * (n + 1) / 2;  // panel buffer n x kPanel
     __shared__ T diag0[kMaxW];
     __shared__ T xs[kMaxW];
     __shared__ T prow[kPanel];
@@ -105,7 +104,7 @@ __global__ void __launch_bounds__(1024) cholinv_kernel(const CholDesc* __restric
 #pragma unroll
             for (int c = 0; c < kPanel; ++c) {
                 if (c < nb && p0 + c <= i) L[pk(i, p0 + c)] = r[c];
-                P[(long long)i * kPanel + c] = (c < nb) ? r[c] : T(0);
+
             }
         }
         __syncthreads();
@@ -131,8 +130,8 @@ __global__ void __launch_bounds__(1024) cholinv_kernel(const CholDesc* __restric
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int ii = t0 + I * 4 + u, jj = t0 + J * 4 + u;
-                        a[u] = (ii < n) ? P[(long long)ii * kPanel + c] : T(0);
-                        b[u] = (jj < n) ? P[(long long)jj * kPanel + c] : T(0);
+                        a[u] = (ii < n && c < nb) ? L[pk(ii, p0 + c)] : T(0);
+                        b[u] = (jj < n && c < nb) ? L[pk(jj, p0 + c)] : T(0);
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
@@ -259,7 +258,7 @@ __global__ void __launch_bounds__(1024) complete_kernel(const CompleteDesc* __re
 
 size_t cholinv_smem_bytes(int wmax, bool fp64) {
     const size_t es = fp64 ? 8 : 4;
-    return ((size_t)wmax * (wmax + 1) / 2 + (size_t)wmax * kPanel) * es;
+    return (size_t)wmax * (wmax + 1) / 2 * es;
 }
 
 void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, bool gram64, double tol,
@@ -267,18 +266,13 @@ void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, 
     if (nfactors == 0) return;
     RKFAC_REQUIRE(wmax <= kMaxW, RKFAC_INVALID_ARGUMENT, "sketch width above 512 is not supported");
     const size_t bytes = cholinv_smem_bytes(wmax, fp64);
-    const bool use_smem = bytes <= 200 * 1024 + (fp64 ? 32 * 1024 : 0);
-    const size_t dyn = use_smem ? bytes : 0;
     const int threads = 1024;
-    if (fp64) {
-        auto k = gram64 ? cholinv_kernel<double, double> : cholinv_kernel<float, double>;
-        RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        k<<<nfactors, threads, dyn, s>>>(d_descs, use_smem ? 1 : 0, tol);
-    } else {
-        auto k = gram64 ? cholinv_kernel<double, float> : cholinv_kernel<float, float>;
-        RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        k<<<nfactors, threads, dyn, s>>>(d_descs, use_smem ? 1 : 0, tol);
-    }
+    auto k = fp64 ? (gram64 ? cholinv_kernel<double, double> : cholinv_kernel<float, double>)
+                  : (gram64 ? cholinv_kernel<double, float> : cholinv_kernel<float, float>);
+    const bool use_smem = bytes <= max_dynamic_smem((const void*)k);
+    const size_t dyn = use_smem ? bytes : 0;
+    RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k<<<nfactors, threads, dyn, s>>>(d_descs, use_smem ? 1 : 0, tol);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

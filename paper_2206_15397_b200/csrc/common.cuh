@@ -65,6 +65,17 @@ __device__ __forceinline__ double gaussian_at(uint64_t seed, uint64_t ctr) {
     return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793238462643383279502884 * u2);
 }
 
+// Largest dynamic shared memory a launch of `kernel` may request on the current device
+// (opt-in per-block limit minus the kernel's static shared memory).
+inline size_t max_dynamic_smem(const void* kernel) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes attr{};
+    if (cudaFuncGetAttributes(&attr, kernel) != cudaSuccess) return 0;
+    return optin > (int)attr.sharedSizeBytes ? (size_t)(optin - (int)attr.sharedSizeBytes) : 0;
+}
+
 // Device buffer with RAII (plan workspaces).
 struct DevBuf {
     void* p = nullptr;

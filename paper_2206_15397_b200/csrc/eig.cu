@@ -353,7 +353,7 @@ void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaSt
     if (nfactors == 0) return;
     RKFAC_REQUIRE(nmax <= kMaxN, RKFAC_INVALID_ARGUMENT, "core size above 512 is not supported");
     const size_t bytes = tridiag_smem_bytes(nmax);
-    const bool use_smem = bytes <= 210 * 1024;
+    const bool use_smem = bytes <= max_dynamic_smem((const void*)tridiag_kernel);
     const size_t dyn = use_smem ? bytes : 0;
     RKFAC_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     tridiag_kernel<<<nfactors, 1024, dyn, s>>>(d_descs, use_smem ? 1 : 0);

@@ -13,6 +13,8 @@
 
 #include "engine.cuh"
 
+#include <cstdlib>
+
 namespace rkfac_b200 {
 
 namespace {
@@ -47,9 +49,11 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
     RKFAC_REQUIRE(n >= 0, RKFAC_INVALID_ARGUMENT, "negative factor count");
     RKFAC_REQUIRE(method == RKFAC_SREVD || method == RKFAC_RSVD, RKFAC_INVALID_ARGUMENT, "unknown method");
     f_.resize(n);
+    const char* simt = std::getenv("RKFAC_SIMT_XQ");
+    use_tc_ = !(simt && simt[0] == '1');
     Carver c;
     struct Offs {
-        size_t B0, B1, G64, G32, L64, L32, flags, chol, core, esc, refl, tau, dvec, evec, evals, scr, piv, z, P,
+        size_t B0, B1, Qh, Ql, Xh, Xl, G64, G32, L64, L32, flags, chol, core, esc, refl, tau, dvec, evec, evals, scr, piv, z, P,
             scale, zflags, bracket;
     };
     std::vector<Offs> offs(n);
@@ -70,8 +74,14 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         wmax_ = std::max(wmax_, F.w);
         rmax_ = std::max(rmax_, F.r);
         Offs& o = offs[i];
-        o.B0 = c.take<float>(w * d);
-        o.B1 = c.take<float>(w * d);
+        F.dp = (int)((d + 31) / 32 * 32);
+        const size_t dp = F.dp;
+        o.B0 = c.take<float>(w * dp);
+        o.B1 = c.take<float>(w * dp);
+        o.Qh = c.take<float>(w * dp);
+        o.Ql = c.take<float>(w * dp);
+        o.Xh = c.take<float>(d * dp);
+        o.Xl = c.take<float>(d * dp);
         o.G64 = c.take<double>(w * w);
         o.G32 = c.take<float>(w * w);
         o.L64 = c.take<double>(w * w);
@@ -98,6 +108,8 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         FactorState& F = f_[i];
         const Offs& o = offs[i];
         F.B0 = at<float>(arena_, o.B0); F.B1 = at<float>(arena_, o.B1);
+        F.Qh = at<float>(arena_, o.Qh); F.Ql = at<float>(arena_, o.Ql);
+        F.Xh = at<float>(arena_, o.Xh); F.Xl = at<float>(arena_, o.Xl);
         F.G64 = at<double>(arena_, o.G64); F.G32 = at<float>(arena_, o.G32);
         F.Linv64 = at<double>(arena_, o.L64); F.Linv32 = at<float>(arena_, o.L32);
         F.flags = at<int>(arena_, o.flags);
@@ -111,13 +123,10 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         F.P = at<float>(arena_, o.P); F.scale = at<float>(arena_, o.scale);
         F.zflags = at<int>(arena_, o.zflags); F.bracket = at<float>(arena_, o.bracket);
     }
-    for (auto& e : ev_) RKFAC_CUDA(cudaEventCreate(&e));
 }
 
 Plan::~Plan() {
-    for (auto& e : ev_)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : xq_ev_) cudaEventDestroy(e);
+    for (auto& e : pool_) cudaEventDestroy(e);
 }
 
 double Plan::xq_flops() const {
@@ -200,12 +209,20 @@ void Plan::build_decomp_stages() {
     for (int i = 0; i < n; ++i) {
         FactorState& F = f_[i];
         OmegaDesc o{};
-        o.d = F.d; o.w = F.w; o.ld = F.d; o.out = F.B1; o.tag = F.tag; o.seed = 0; o.ctr0 = 0; o.offset = off;
+        o.d = F.d; o.w = F.w; o.ld = F.dp; o.out = F.B1; o.tag = F.tag; o.seed = 0; o.ctr0 = 0; o.offset = off;
         off += (long long)F.d * F.w;
         omega_[i] = o;
     }
     omega_total_ = off;
     upload(d_omega_, omega_);
+    std::vector<SplitDesc> sx;
+    long long sx_off = 0;
+    for (auto& F : f_) {
+        sx.push_back(SplitDesc{F.X, F.Xh, F.Xl, F.d, F.d, F.ldx, F.dp, sx_off});
+        sx_off += (long long)F.d * F.d;
+    }
+    upload(d_split_x_, sx);
+    split_x_total_ = sx_off;
 
     for (int dir = 0; dir < 2; ++dir) {
         xq_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
@@ -215,35 +232,44 @@ void Plan::build_decomp_stages() {
         tri32_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
         core_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
         lift_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
+        xq_tc_[dir] = std::make_unique<TcXQ>();
         std::vector<CompleteDesc> comp;
+        std::vector<SplitDesc> sq;
+        long long sq_off = 0;
         for (auto& F : f_) {
             float* Bd = dir == 0 ? F.B0 : F.B1;  // Y (output of xq_[dir]); src of orth_[dir]
             float* Bo = dir == 0 ? F.B1 : F.B0;  // Q
             // Y^T = (X Q)^T : M=d, N=w, K=d
-            xq_[dir]->add(GemmBatch::make(F.d, F.w, F.d, F.X, F.ldx, 0, Bo, F.d, 1, Bd, F.d, 1));
+            xq_[dir]->add(GemmBatch::make(F.d, F.w, F.d, F.X, F.ldx, 0, Bo, F.dp, 1, Bd, F.dp, 1));
+            xq_tc_[dir]->add(TcOperand{F.Xh, F.Xl, F.dp}, TcOperand{F.Qh, F.Ql, F.dp}, F.d, F.w, F.d, Bd, F.dp);
+            sq.push_back(SplitDesc{Bo, F.Qh, F.Ql, F.w, F.d, F.dp, F.dp, sq_off});
+            sq_off += (long long)F.w * F.d;
             // orth of B[dir] into B[dir^1]: G = Y^T Y (w x w), then Q^T = Linv Y^T
-            GemmDesc g64 = GemmBatch::make(F.w, F.w, F.d, Bd, F.d, 0, Bd, F.d, 1, F.G64, F.w, 0);
+            GemmDesc g64 = GemmBatch::make(F.w, F.w, F.d, Bd, F.dp, 0, Bd, F.dp, 1, F.G64, F.w, 0);
             g64.ksplit = choose_ksplit(F.w, F.w, F.d, 64, 64);
             gram64_[dir]->add(g64);
-            tri64_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv64, F.w, 0, Bd, F.d, 0, Bo, F.d, 0));
-            GemmDesc g32 = GemmBatch::make(F.w, F.w, F.d, Bd, F.d, 0, Bd, F.d, 1, F.G32, F.w, 0);
+            tri64_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv64, F.w, 0, Bd, F.dp, 0, Bo, F.dp, 0));
+            GemmDesc g32 = GemmBatch::make(F.w, F.w, F.d, Bd, F.dp, 0, Bd, F.dp, 1, F.G32, F.w, 0);
             g32.ksplit = choose_ksplit(F.w, F.w, F.d, 128, 128);
             gram32_[dir]->add(g32);
-            tri32_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv32, F.w, 0, Bd, F.d, 0, Bo, F.d, 0));
-            comp.push_back(CompleteDesc{F.w, F.d, F.d, Bo, F.flags, F.flags + F.w});
+            tri32_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv32, F.w, 0, Bd, F.dp, 0, Bo, F.dp, 0));
+            comp.push_back(CompleteDesc{F.w, F.d, F.dp, Bo, F.flags, F.flags + F.w});
             // core: srevd C = Q^T (X Q) (rnla.hpp:97); rsvd_psd Gram B B^T = Y^T Y (eig.hpp:251)
             const float* Aop = method_ == RKFAC_SREVD ? Bo : Bd;
-            GemmDesc cd = GemmBatch::make(F.w, F.w, F.d, Aop, F.d, 0, Bd, F.d, 1, F.core, F.w, 0);
+            GemmDesc cd = GemmBatch::make(F.w, F.w, F.d, Aop, F.dp, 0, Bd, F.dp, 1, F.core, F.w, 0);
             cd.ksplit = choose_ksplit(F.w, F.w, F.d, 128, 128);
             core_[dir]->add(cd);
             // lift: srevd U^T = P_r^T Q^T (rnla.hpp:101); rsvd U^T = diag(1/s) P_r^T Y^T (eig.hpp:260-266)
             const float* Bop = method_ == RKFAC_SREVD ? Bo : Bd;
-            GemmDesc ld = GemmBatch::make(F.r, F.d, F.w, F.P, F.r, 1, Bop, F.d, 0, F.Ut, F.ldu, 0);
+            GemmDesc ld = GemmBatch::make(F.r, F.d, F.w, F.P, F.r, 1, Bop, F.dp, 0, F.Ut, F.ldu, 0);
             if (method_ == RKFAC_RSVD) ld.rs = F.scale;
             lift_[dir]->add(ld);
         }
         // complete_[dir] completes the output of orth_from(dir) (which is B[dir^1]).
         upload(d_complete_[dir], comp);
+        upload(d_split_q_[dir], sq);
+        split_q_total_ = sq_off;
+        xq_tc_[dir]->finalize();
         xq_[dir]->finalize(); gram64_[dir]->finalize(); tri64_[dir]->finalize();
         gram32_[dir]->finalize(); tri32_[dir]->finalize(); core_[dir]->finalize(); lift_[dir]->finalize();
     }
@@ -329,14 +355,42 @@ void Plan::orth(int src, int dst, bool fp64, cudaStream_t s) {
     launch_complete(d_complete_[src].as<CompleteDesc>(), n, s);
 }
 
-void Plan::record(int idx, bool) {
-    if (timing_) RKFAC_CUDA(cudaEventRecord(ev_[idx], ctx_->stream));
+// ---- stage timing: CUDA events from a pool, recorded on the context stream, harvested after the caller syncs
+// (no host synchronisation inside a step).  Kinds: see TimingKind.
+void Plan::mark(int kind, bool begin) {
+    if (!timing_) return;
+    if (pool_used_ == pool_.size()) {
+        cudaEvent_t e;
+        RKFAC_CUDA(cudaEventCreate(&e));
+        pool_.push_back(e);
+    }
+    const size_t idx = pool_used_++;
+    RKFAC_CUDA(cudaEventRecord(pool_[idx], ctx_->stream));
+    if (begin) open_[kind] = idx;
+    else recs_.push_back({kind, open_[kind], idx});
+}
+
+void Plan::timing_reset() {
+    pool_used_ = 0;
+    recs_.clear();
+}
+
+void Plan::timing_report(float* sums, int* counts) const {
+    for (int k = 0; k < kTimingKinds; ++k) { sums[k] = 0.f; counts[k] = 0; }
+    for (const auto& r : recs_) {
+        float t = 0.f;
+        RKFAC_CUDA(cudaEventElapsedTime(&t, pool_[r.b], pool_[r.e]));
+        sums[r.kind] += t;
+        counts[r.kind] += 1;
+    }
 }
 
 void Plan::ea_update(double rho, double scale) {
     RKFAC_REQUIRE(factors_bound_ && samples_bound_, RKFAC_INVALID_ARGUMENT, "factors/samples not bound");
     if (rho != ea_rho_ || scale != ea_scale_) build_ea_stage(rho, scale);
+    mark(kEA, true);
     ea_->launch(ctx_->stream);
+    mark(kEA, false);
 }
 
 void Plan::decompose(int mode, uint64_t root, uint64_t step) {
@@ -348,54 +402,42 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step) {
     for (auto& F : f_) qmax = std::max(qmax, F.q);
     for (auto& F : f_)
         RKFAC_REQUIRE(F.q == qmax, RKFAC_INVALID_ARGUMENT, "all factors of a plan share power_iters");
+    mark(kDecompose, true);
     launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
     int cur_q = 1;  // Q lives in B[cur_q]
     const int north = 2 * qmax + 1;
     bool last_fp64 = false;
-    const size_t nev = 2 * (size_t)(north + 1);
-    if (timing_ && xq_ev_.size() < nev) {
-        for (size_t i = xq_ev_.size(); i < nev; ++i) {
-            cudaEvent_t e;
-            RKFAC_CUDA(cudaEventCreate(&e));
-            xq_ev_.push_back(e);
-        }
-    }
-    if (timing_) RKFAC_CUDA(cudaEventRecord(ev_[4], s));
-    int xi = 0;
+    if (use_tc_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);
     auto timed_xq = [&](int y) {
-        if (timing_) RKFAC_CUDA(cudaEventRecord(xq_ev_[xi++], s));
-        xq_[y]->launch(s);
-        if (timing_) RKFAC_CUDA(cudaEventRecord(xq_ev_[xi++], s));
+        if (use_tc_) launch_split(d_split_q_[y].as<SplitDesc>(), n, split_q_total_, s);
+        mark(kXQ, true);
+        if (use_tc_) xq_tc_[y]->launch(s); else xq_[y]->launch(s);
+        mark(kXQ, false);
     };
     for (int o = 0; o < north; ++o) {
         const int y = cur_q ^ 1;
         timed_xq(y);
         last_fp64 = o < n_fp64_orth_;
+        mark(kOrth, true);
         orth(y, cur_q, last_fp64, s);
+        mark(kOrth, false);
     }
     if (!last_fp64) {  // CholeskyQR2: second pass so the final basis is orthonormal to FP32 rounding
+        mark(kOrth, true);
         orth(cur_q, cur_q ^ 1, false, s);
+        mark(kOrth, false);
         cur_q ^= 1;
     }
     const int y = cur_q ^ 1;
     timed_xq(y);
+    mark(kEig, true);
     core_[y]->launch(s);
     launch_eig(d_eig_.as<EigDesc>(), n, wmax_, rmax_, s);
     launch_post(d_post_.as<PostDesc>(), n, s);
     lift_[y]->launch(s);
     if (method_ == RKFAC_RSVD) launch_complete(d_complete_u_.as<CompleteDesc>(), n, s);
-    if (timing_) {
-        RKFAC_CUDA(cudaEventRecord(ev_[5], s));
-        RKFAC_CUDA(cudaEventSynchronize(ev_[5]));
-        RKFAC_CUDA(cudaEventElapsedTime(&stage_ms_[1], ev_[4], ev_[5]));
-        float xq_ms = 0.f;
-        for (int i = 0; i + 1 < xi; i += 2) {
-            float t = 0.f;
-            RKFAC_CUDA(cudaEventElapsedTime(&t, xq_ev_[i], xq_ev_[i + 1]));
-            xq_ms += t;
-        }
-        stage_ms_[3] = xq_ms;
-    }
+    mark(kEig, false);
+    mark(kDecompose, false);
 }
 
 void Plan::precondition(double lambda) {
@@ -404,27 +446,19 @@ void Plan::precondition(double lambda) {
     if (layers_.empty()) return;
     if (lambda != ap_lambda_) build_apply_stages(lambda);
     cudaStream_t s = ctx_->stream;
+    mark(kApply, true);
     launch_bracket(d_bracket_.as<BracketDesc>(), nfactors(), lambda, s);
     for (auto& a : ap_) a->launch(s);
+    mark(kApply, false);
 }
 
 void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double lambda) {
     RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
-    cudaStream_t s = ctx_->stream;
-    if (timing_) RKFAC_CUDA(cudaEventRecord(ev_[0], s));
+    mark(kStep, true);
     if (samples_bound_) ea_update(rho, scale);
-    if (timing_) RKFAC_CUDA(cudaEventRecord(ev_[1], s));
     decompose(1, root, stp);
-    if (timing_) RKFAC_CUDA(cudaEventRecord(ev_[2], s));
     precondition(lambda);
-    if (timing_) {
-        RKFAC_CUDA(cudaEventRecord(ev_[3], s));
-        RKFAC_CUDA(cudaEventSynchronize(ev_[3]));
-        RKFAC_CUDA(cudaEventElapsedTime(&stage_ms_[0], ev_[0], ev_[1]));
-        RKFAC_CUDA(cudaEventElapsedTime(&stage_ms_[2], ev_[2], ev_[3]));
-    }
+    mark(kStep, false);
 }
-
-void Plan::stage_ms(float* out4) const { std::memcpy(out4, stage_ms_, sizeof(stage_ms_)); }
 
 }  // namespace rkfac_b200

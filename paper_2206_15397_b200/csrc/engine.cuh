@@ -10,6 +10,7 @@
 
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "tc_gemm.cuh"
 
 namespace rkfac_b200 {
 
@@ -17,6 +18,7 @@ struct Context;
 
 struct FactorState {
     int d = 0, r = 0, p = 0, q = 0, w = 0;  // clamped r, p; w = r + p
+    int dp = 0;                              // d rounded up to 32: pitch of internal w x d / d x d buffers (TMA)
     // bound (caller-owned)
     float* X = nullptr;     // d x d
     long long ldx = 0;
@@ -27,7 +29,9 @@ struct FactorState {
     long long n = 0;
     uint64_t tag = 0;
     // plan-owned workspace (carved from the arena)
-    float *B0 = nullptr, *B1 = nullptr;  // w x d each (ld = d)
+    float *B0 = nullptr, *B1 = nullptr;  // w x d each (ld = dp)
+    float *Qh = nullptr, *Ql = nullptr;  // TF32 hi/lo planes of the current Q^T (w x d, ld = dp)
+    float *Xh = nullptr, *Xl = nullptr;  // TF32 hi/lo planes of X (d x d, ld = dp)
     double* G64 = nullptr;               // w x w (Gram, FP64)
     float* G32 = nullptr;                // w x w (Gram, FP32)
     double* Linv64 = nullptr;
@@ -75,8 +79,11 @@ class Plan {
     void precondition(double lambda);
     void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
 
-    void set_timing(bool on) { timing_ = on; }
-    void stage_ms(float* out4) const;
+    enum TimingKind { kEA = 0, kDecompose = 1, kApply = 2, kXQ = 3, kOrth = 4, kEig = 5, kStep = 6, kTimingKinds = 7 };
+    void set_timing(bool on) { timing_ = on; timing_reset(); }
+    void timing_reset();
+    // Sums (ms) and counts of each timed region since the last reset; call after the stream is synchronised.
+    void timing_report(float* sums, int* counts) const;
     bool has_samples() const { return samples_bound_; }
     bool has_layers() const { return !layers_.empty(); }
 
@@ -88,7 +95,7 @@ class Plan {
     void build_ea_stage(double rho, double scale);
     void build_apply_stages(double lambda);
     void orth(int src, int dst, bool fp64, cudaStream_t s);
-    void record(int idx, bool begin);
+    void mark(int kind, bool begin);
 
     Context* ctx_;
     int method_;
@@ -103,6 +110,10 @@ class Plan {
     std::unique_ptr<GemmBatch> core_[2];      // core from (Q in B[dir^1], Y in B[dir])
     std::unique_ptr<GemmBatch> lift_[2];
     std::unique_ptr<GemmBatch> ea_;
+    std::unique_ptr<TcXQ> xq_tc_[2];
+    DevBuf d_split_x_, d_split_q_[2];
+    long long split_x_total_ = 0, split_q_total_ = 0;
+    bool use_tc_ = true;
     std::unique_ptr<GemmBatch> ap_[4];
     DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
     std::vector<OmegaDesc> omega_;
@@ -112,9 +123,11 @@ class Plan {
     int n_fp64_orth_ = 2;
 
     bool timing_ = false;
-    cudaEvent_t ev_[8] = {};
-    std::vector<cudaEvent_t> xq_ev_;
-    float stage_ms_[4] = {0, 0, 0, 0};
+    struct Rec { int kind; size_t b, e; };
+    std::vector<cudaEvent_t> pool_;
+    size_t pool_used_ = 0;
+    size_t open_[kTimingKinds] = {};
+    std::vector<Rec> recs_;
 };
 
 struct Context {
