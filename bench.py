@@ -326,6 +326,7 @@ def run_ours(args, wl):
     step.set_timing(True)
     launches0 = ctx.launches()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             reset()
@@ -333,6 +334,7 @@ def run_ours(args, wl):
             one_step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     launches = ctx.launches() - launches0

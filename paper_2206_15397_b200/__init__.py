@@ -178,6 +178,9 @@ class Context:
 
 def context(device: Optional[int] = None) -> Context:
     torch = _torch()
+    load_library()
+    if not torch.cuda.is_available():
+        raise CudaError("rkfac_b200 needs a CUDA device (sm_100); there is no CPU fallback")
     dev = torch.cuda.current_device() if device is None else device
     if dev not in _contexts:
         _contexts[dev] = Context(dev)

@@ -51,6 +51,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
     f_.resize(n);
     const char* simt = std::getenv("RKFAC_SIMT_XQ");
     use_tc_ = !(simt && simt[0] == '1');
+    if (const char* nf = std::getenv("RKFAC_FP64_ORTHS")) n_fp64_orth_ = std::atoi(nf);
     Carver c;
     struct Offs {
         size_t B0, B1, Qh, Ql, Xh, Xl, G64, G32, L64, L32, flags, chol, core, esc, refl, tau, dvec, evec, evals, scr, piv, z, P,

@@ -120,7 +120,10 @@ class Plan {
     long long omega_total_ = 0;
     int wmax_ = 0, rmax_ = 0;
     double ea_rho_ = -1, ea_scale_ = -1, ap_lambda_ = -1;
-    int n_fp64_orth_ = 2;
+    // Orthonormalisations done in FP64 (Gram, Cholesky, Y L^-T): only the first sketch Y0 = X Omega is
+    // ill-conditioned enough (kappa ~1e4) to break FP32 CholeskyQR; measured: 1 vs 2 FP64 orths give
+    // the same parity error, 0 gives eigenvalue errors of ~5e-2.
+    int n_fp64_orth_ = 1;
 
     bool timing_ = false;
     struct Rec { int kind; size_t b, e; };

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -267,7 +268,7 @@ xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict_
 // ------------------------------------------------------------------------------ hi/lo split producers
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-__global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long long total) {
+__global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long long total, int raw_hi) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         int lo = 0, hi = n - 1;
@@ -280,7 +281,7 @@ __global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long lo
         const int r = (int)(local / sd.cols), c = (int)(local - (long long)r * sd.cols);
         const float x = sd.src[(long long)r * sd.lds + c];
         const float h = tf32_trunc(x);
-        sd.hi[(long long)r * sd.ldd + c] = h;
+        sd.hi[(long long)r * sd.ldd + c] = raw_hi ? x : h;
         sd.lo[(long long)r * sd.ldd + c] = x - h;
     }
 }
@@ -391,7 +392,8 @@ double TcXQ::flops() const {
 void launch_split(const SplitDesc* d_descs, int n, long long total, cudaStream_t s) {
     if (total == 0) return;
     const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
-    split_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
+    static const int raw_hi = [] { const char* e = std::getenv("RKFAC_RAW_HI"); return e && e[0] == '1'; }();
+    split_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total, raw_hi);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }
