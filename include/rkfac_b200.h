@@ -111,6 +111,10 @@ int64_t rkfac_plan_rank(rkfac_plan_t plan, int f);
  * contiguous).  dvals[f]: rank_f floats. */
 int rkfac_plan_bind_factors(rkfac_plan_t plan, float* const* factors_dev, float* const* bases_t_dev,
                             float* const* dvals_dev);
+/* As rkfac_plan_bind_factors with explicit row pitches (elements).  Pitches that are multiples of 4 with 16-byte
+ * aligned bases let the EA update and the X*Q products feed the factor to TMA directly (no padded copy). */
+int rkfac_plan_bind_factors_ld(rkfac_plan_t plan, float* const* factors_dev, const int64_t* ld_factors,
+                               float* const* bases_t_dev, const int64_t* ld_bases, float* const* dvals_dev);
 /* samples[f]: d_f x n_f (ld = n_f), the m argument of ea_update. */
 int rkfac_plan_bind_samples(rkfac_plan_t plan, const float* const* samples_dev, const int64_t* n);
 /* Layer l preconditions grads[l] (d_G x d_A, ld = d_A) with A-factor a_idx[l] and G-factor g_idx[l] into

@@ -100,6 +100,8 @@ SIGNATURES = {
     "rkfac_plan_destroy": (C.c_int, [_vp]),
     "rkfac_plan_rank": (_c_i64, [_vp, C.c_int]),
     "rkfac_plan_bind_factors": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+    "rkfac_plan_bind_factors_ld": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_c_i64), C.POINTER(_vp),
+                                             C.POINTER(_c_i64), C.POINTER(_vp)]),
     "rkfac_plan_bind_samples": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_c_i64)]),
     "rkfac_plan_bind_layers": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(_vp),
                                          C.POINTER(_vp), C.POINTER(_vp)]),
@@ -400,13 +402,19 @@ class BatchedStep:
         self.h = h
         dev = torch.device("cuda", self.device)
         self.ranks = [int(lib.rkfac_plan_rank(h, f)) for f in range(len(dims))]
+        lds = []
         for f, d in enumerate(dims):
-            self.factors.append(torch.zeros(d, d, device=dev))
+            # factors live in row-pitch-padded storage (pitch multiple of 32 floats) so the EA update and the
+            # X*Q products feed them to TMA directly; self.factors[f] is the d x d view
+            ld = (d + 31) // 32 * 32
+            lds.append(ld)
+            self.factors.append(torch.zeros(d, ld, device=dev)[:, :d])
             self.bases_t.append(torch.zeros(self.ranks[f], d, device=dev))
             self.dvals.append(torch.zeros(self.ranks[f], device=dev))
         arr = lambda ts: (_vp * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
-        _check(lib.rkfac_plan_bind_factors(h, arr(self.factors), arr(self.bases_t), arr(self.dvals)), self.ctx.h,
-               "bind_factors")
+        ldf = (_c_i64 * len(dims))(*lds)
+        _check(lib.rkfac_plan_bind_factors_ld(h, arr(self.factors), ldf, arr(self.bases_t), None, arr(self.dvals)),
+               self.ctx.h, "bind_factors")
         if self.factor_indices is not None:
             tags = (_c_u64 * len(dims))(*[int(t) for t in self.factor_indices])
             _check(lib.rkfac_plan_set_tags(h, tags), self.ctx.h, "set_tags")

@@ -254,6 +254,20 @@ int rkfac_plan_bind_factors(rkfac_plan_t plan, float* const* factors, float* con
     });
 }
 
+int rkfac_plan_bind_factors_ld(rkfac_plan_t plan, float* const* factors, const int64_t* ld_factors,
+                               float* const* bases_t, const int64_t* ld_bases, float* const* dvals) {
+    return guarded(plan ? plan->ctx : nullptr, [&] {
+        RKFAC_REQUIRE(plan && factors && bases_t && dvals, RKFAC_INVALID_ARGUMENT, "null argument");
+        const int n = plan->p->nfactors();
+        std::vector<long long> lx(n), lu(n);
+        for (int i = 0; i < n; ++i) {
+            lx[i] = ld_factors ? ld_factors[i] : plan->p->factor(i).d;
+            lu[i] = ld_bases ? ld_bases[i] : plan->p->factor(i).d;
+        }
+        plan->p->bind_factors(factors, lx.data(), bases_t, lu.data(), dvals);
+    });
+}
+
 int rkfac_plan_bind_samples(rkfac_plan_t plan, const float* const* samples, const int64_t* n) {
     return guarded(plan ? plan->ctx : nullptr, [&] {
         RKFAC_REQUIRE(plan && samples && n, RKFAC_INVALID_ARGUMENT, "null argument");

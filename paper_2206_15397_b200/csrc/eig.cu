@@ -42,13 +42,16 @@ __device__ double block_sum_d(double v, double* red) {
 }
 
 // ---------------------------------------------------------------------------------------------- tridiag
-__global__ void __launch_bounds__(1024) tridiag_kernel(const EigDesc* __restrict__ descs, int use_smem) {
+template <bool kSmem>  // compile-time storage choice: LDS/STS instead of generic LD/ST
+__global__ void __launch_bounds__(1024) tridiag_kernel(const EigDesc* __restrict__ descs) {
     const EigDesc& ed = descs[blockIdx.x];
     const int n = ed.n;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* A = use_smem ? reinterpret_cast<double*>(smem_raw) : ed.scratch;
+    double* A;
+    if constexpr (kSmem) A = reinterpret_cast<double*>(smem_raw);
+    else A = ed.scratch;
     __shared__ double v[kMaxN], p[kMaxN], red[33];
 
     // Load the symmetrised lower triangle of the FP32 core.
@@ -187,15 +190,52 @@ __global__ void __launch_bounds__(256) tdeig_kernel(const EigDesc* __restrict__ 
     __syncthreads();
     const double pivmin = s_pivmin, tnorm = s_tnorm;
 
-    // Bisection for the k-th largest eigenvalue (ascending index n-1-k).
+    // Multisection for the k-th largest eigenvalue (ascending index n-1-k): 4 Sturm counts per iteration run as
+    // independent chains (their divisions overlap), shrinking the bracket 5x per iteration instead of 2x.
     for (int k = tid; k < r; k += blockDim.x) {
         const int idx = n - 1 - k;
         double lo = s_lo, hi = s_hi;
         const double abstol = 4.0 * DBL_EPSILON * tnorm;
-        for (int it = 0; it < 200; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + abstol || mid == lo || mid == hi) break;
-            if (sturm_count(d, e2, n, mid, pivmin) <= idx) lo = mid; else hi = mid;
+        for (int it = 0; it < 100; ++it) {
+            if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + abstol) break;
+            const double h = (hi - lo) * 0.2;
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = lo + h * (u + 1);
+            if (x[0] <= lo || x[3] >= hi) {  // bracket at the resolution of doubles: plain bisection step
+                const double mid = 0.5 * (lo + hi);
+                if (mid == lo || mid == hi) break;
+                if (sturm_count(d, e2, n, mid, pivmin) <= idx) lo = mid; else hi = mid;
+                continue;
+            }
+            double q[4];
+            int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                q[u] = d[0] - x[u];
+                if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+                cnt[u] += q[u] < 0.0;
+            }
+            for (int i = 1; i < n; ++i) {
+                const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    q[u] = di - x[u] - ei / q[u];
+                    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+                    cnt[u] += q[u] < 0.0;
+                }
+            }
+            // counts are nondecreasing in x: the eigenvalue lies in the first sub-interval whose right end has
+            // more than idx eigenvalues below it
+            double nlo = lo, nhi = hi;
+#pragma unroll
+            for (int u = 3; u >= 0; --u)
+                if (cnt[u] <= idx) { nlo = x[u]; break; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (cnt[u] > idx) { nhi = x[u]; break; }
+            lo = nlo;
+            hi = nhi;
         }
         lam[k] = 0.5 * (lo + hi);
     }
@@ -311,33 +351,52 @@ __global__ void __launch_bounds__(256) backxform_kernel(const EigDesc* __restric
     const int nc = min(kBxCols, r - c0);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* Zs = reinterpret_cast<double*>(smem_raw);  // [n][kBxCols]
-    __shared__ double vk[kMaxN], dots[kBxCols];
-    const int tid = threadIdx.x;
+    __shared__ double vk[2][kMaxN], dots[kBxCols];
+    const int tid = threadIdx.x;  // blockDim.x == 256: two reflector entries per thread (n <= 512)
     for (long long e = tid; e < (long long)n * kBxCols; e += blockDim.x) {
         const int i = (int)(e / kBxCols), c = (int)(e % kBxCols);
         Zs[e] = (c < nc) ? ed.z[(long long)i * r + c0 + c] : 0.0;
     }
+    // The reflector of step k-1 is fetched into registers while step k computes (its global load latency was
+    // the serial critical path: one L2 round trip per reflector).
+    int buf = 0;
+    double tau = 0.0;
+    if (n >= 3) {
+        const int k0 = n - 3, m0 = n - k0 - 1;
+        for (int t = tid; t < m0; t += blockDim.x) vk[0][t] = ed.refl[(long long)k0 * n + t];
+        tau = ed.tau[k0];
+    }
     __syncthreads();
     for (int k = n - 3; k >= 0; --k) {
-        const double tau = ed.tau[k];
-        if (tau == 0.0) continue;
         const int m = n - k - 1;
-        for (int t = tid; t < m; t += blockDim.x) vk[t] = ed.refl[(long long)k * n + t];
-        __syncthreads();
-        // dots[c] = v^T Z[k+1:, c]; 8 threads per column.
-        {
-            const int c = tid / 8, seg = tid % 8;
-            double s = 0.0;
-            for (int t = seg; t < m; t += 8) s += vk[t] * Zs[(long long)(k + 1 + t) * kBxCols + c];
-            for (int o = 4; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, 8);
-            if (seg == 0) dots[c] = tau * s;
+        double pf0 = 0.0, pf1 = 0.0, tau_next = 0.0;
+        if (k > 0) {
+            const long long base = (long long)(k - 1) * n;
+            if (tid < m + 1) pf0 = ed.refl[base + tid];
+            if (tid + 256 < m + 1) pf1 = ed.refl[base + tid + 256];
+            tau_next = ed.tau[k - 1];
         }
-        __syncthreads();
-        for (long long e = tid; e < (long long)m * kBxCols; e += blockDim.x) {
-            const int t = (int)(e / kBxCols), c = (int)(e % kBxCols);
-            Zs[(long long)(k + 1 + t) * kBxCols + c] -= dots[c] * vk[t];
+        if (tau != 0.0) {
+            const double* v = vk[buf];
+            // dots[c] = v^T Z[k+1:, c]; 8 threads per column.
+            {
+                const int c = tid / 8, seg = tid % 8;
+                double s = 0.0;
+                for (int t = seg; t < m; t += 8) s += v[t] * Zs[(long long)(k + 1 + t) * kBxCols + c];
+                for (int o = 4; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, 8);
+                if (seg == 0) dots[c] = tau * s;
+            }
+            __syncthreads();
+            for (long long e = tid; e < (long long)m * kBxCols; e += blockDim.x) {
+                const int t = (int)(e / kBxCols), c = (int)(e % kBxCols);
+                Zs[(long long)(k + 1 + t) * kBxCols + c] -= dots[c] * v[t];
+            }
         }
+        vk[buf ^ 1][tid] = pf0;
+        if (tid + 256 < kMaxN) vk[buf ^ 1][tid + 256] = pf1;
         __syncthreads();
+        buf ^= 1;
+        tau = tau_next;
     }
     for (long long e = tid; e < (long long)n * kBxCols; e += blockDim.x) {
         const int i = (int)(e / kBxCols), c = (int)(e % kBxCols);
@@ -353,10 +412,11 @@ void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaSt
     if (nfactors == 0) return;
     RKFAC_REQUIRE(nmax <= kMaxN, RKFAC_INVALID_ARGUMENT, "core size above 512 is not supported");
     const size_t bytes = tridiag_smem_bytes(nmax);
-    const bool use_smem = bytes <= max_dynamic_smem((const void*)tridiag_kernel);
+    const bool use_smem = bytes <= max_dynamic_smem((const void*)tridiag_kernel<true>);
+    auto k = use_smem ? tridiag_kernel<true> : tridiag_kernel<false>;
     const size_t dyn = use_smem ? bytes : 0;
-    RKFAC_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    tridiag_kernel<<<nfactors, 1024, dyn, s>>>(d_descs, use_smem ? 1 : 0);
+    RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k<<<nfactors, 1024, dyn, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
     tdeig_kernel<<<nfactors, 256, 0, s>>>(d_descs);

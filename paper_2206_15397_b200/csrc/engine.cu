@@ -1,19 +1,21 @@
 // engine.cu -- Plan: workspace layout and stage orchestration of the batched rand-K-FAC step.
 //
-// Data layout in HBM (per factor f, d = dim, w = r + p after clamping, rnla.hpp:35-43):
-//   X_f        d x d FP32 EA factor (caller-owned, exactly symmetric)
-//   B0, B1     w x d FP32: the sketch Y^T and the orthonormal basis Q^T, ping-ponged (basis vectors contiguous:
-//              coalesced epilogue stores, K-major operands for the next product)
-//   G, Linv    w x w Gram and inverse Cholesky factor (FP64 for the first orthonormalisations, FP32 after)
+// Data layout in HBM (per factor f, d = dim, w = r + p after clamping, rnla.hpp:35-43; dp = d rounded up to 32,
+// wp = w rounded up to 4 so every row pitch is a legal TMA stride):
+//   X_f        d x d FP32 EA factor (caller-owned, exactly symmetric) + its TF32 lo plane Xl (written by the EA
+//              epilogue, or by a split pass when the factor was changed outside a step)
+//   S[0],S[1]  ping-pong sketch / basis roles, each in four planes: T = w x d (basis vectors contiguous: the
+//              K-major operand of X*Q, Y^T Y and Q^T Y), R = d x w (the K-major operand of Y L^-T), and the TF32
+//              lo planes of both (3xTF32 operands); every producer writes all four in its epilogue
+//   G, Linv    w x w Gram and inverse Cholesky factor (FP64 for the first orthonormalisation, FP32 after)
 //   core       w x w FP32 projected matrix (srevd: Q^T X Q, rnla.hpp:97; rsvd_psd: B B^T, eig.hpp:251)
 //   eig        FP64 tridiagonal workspace, P (w x r FP32) eigenvectors of the core
 //   Ut         r x d FP32 caller-owned U^T, dvals r FP32 (LowRankEig, rnla.hpp:17-24)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.cuh"
-
-#include <cstdlib>
 
 namespace rkfac_b200 {
 
@@ -43,19 +45,20 @@ void upload(DevBuf& buf, const std::vector<T>& v) {
 constexpr double kTol64 = 1e-13;  // relative pivot floor for rank deficiency, FP64 Gram
 constexpr double kTol32 = 1e-5;   // FP32 Gram (see cholqr.cu)
 
+TcOut out_t(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 1; return o; }
+TcOut out_r(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 0; return o; }
+
 }  // namespace
 
 Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ctx_(ctx), method_(method) {
     RKFAC_REQUIRE(n >= 0, RKFAC_INVALID_ARGUMENT, "negative factor count");
     RKFAC_REQUIRE(method == RKFAC_SREVD || method == RKFAC_RSVD, RKFAC_INVALID_ARGUMENT, "unknown method");
     f_.resize(n);
-    const char* simt = std::getenv("RKFAC_SIMT_XQ");
-    use_tc_ = !(simt && simt[0] == '1');
     if (const char* nf = std::getenv("RKFAC_FP64_ORTHS")) n_fp64_orth_ = std::atoi(nf);
     Carver c;
     struct Offs {
-        size_t B0, B1, Qh, Ql, Xh, Xl, G64, G32, L64, L32, flags, chol, core, esc, refl, tau, dvec, evec, evals, scr, piv, z, P,
-            scale, zflags, bracket;
+        size_t S[2][4], Xc, Xl, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
+            scr, piv, z, P, scale, zflags, bracket;
     };
     std::vector<Offs> offs(n);
     for (int i = 0; i < n; ++i) {
@@ -70,25 +73,28 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         else if (r + p > ds.dim) p = ds.dim - r;
         F.r = (int)r; F.p = (int)p; F.q = (int)ds.power_iters; F.w = (int)(r + p);
         F.tag = (uint64_t)i;
-        const size_t w = F.w, d = F.d, rr = F.r;
-        RKFAC_REQUIRE(w <= 512, RKFAC_INVALID_ARGUMENT, "sketch width r+p above 512 is not supported");
+        F.dp = (F.d + 31) / 32 * 32;
+        F.wp = (F.w + 3) / 4 * 4;
+        RKFAC_REQUIRE(F.w <= 512, RKFAC_INVALID_ARGUMENT, "sketch width r+p above 512 is not supported");
         wmax_ = std::max(wmax_, F.w);
         rmax_ = std::max(rmax_, F.r);
+        const size_t w = F.w, d = F.d, rr = F.r, dp = F.dp, wp = F.wp;
         Offs& o = offs[i];
-        F.dp = (int)((d + 31) / 32 * 32);
-        const size_t dp = F.dp;
-        o.B0 = c.take<float>(w * dp);
-        o.B1 = c.take<float>(w * dp);
-        o.Qh = c.take<float>(w * dp);
-        o.Ql = c.take<float>(w * dp);
-        o.Xh = c.take<float>(d * dp);
+        for (int s = 0; s < 2; ++s) {
+            o.S[s][0] = c.take<float>(w * dp);
+            o.S[s][1] = c.take<float>(w * dp);
+            o.S[s][2] = c.take<float>(d * wp);
+            o.S[s][3] = c.take<float>(d * wp);
+        }
+        o.Xc = c.take<float>(d * dp);
         o.Xl = c.take<float>(d * dp);
         o.G64 = c.take<double>(w * w);
-        o.G32 = c.take<float>(w * w);
-        o.L64 = c.take<double>(w * w);
-        o.L32 = c.take<float>(w * w);
+        o.G32 = c.take<float>(w * wp);
+        o.L64 = c.take<double>(w * wp);
+        o.L32 = c.take<float>(w * wp);
+        o.L32lo = c.take<float>(w * wp);
         o.flags = c.take<int>(w + 1);
-        o.chol = c.take<double>(w * (w + 1) / 2 + w * 8);
+        o.chol = c.take<double>(w * (w + 1) / 2 + 4 * w);  // padded packed triangle (cholqr.cu prow)
         o.core = c.take<float>(w * w);
         o.esc = c.take<double>(w * (w + 1) / 2);
         o.refl = c.take<double>(w * w);
@@ -105,14 +111,20 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         o.bracket = c.take<float>(rr);
     }
     arena_.alloc(c.off);
+    RKFAC_CUDA(cudaMemset(arena_.p, 0, c.off));
     for (int i = 0; i < n; ++i) {
         FactorState& F = f_[i];
         const Offs& o = offs[i];
-        F.B0 = at<float>(arena_, o.B0); F.B1 = at<float>(arena_, o.B1);
-        F.Qh = at<float>(arena_, o.Qh); F.Ql = at<float>(arena_, o.Ql);
-        F.Xh = at<float>(arena_, o.Xh); F.Xl = at<float>(arena_, o.Xl);
+        for (int s = 0; s < 2; ++s) {
+            F.S[s].T = at<float>(arena_, o.S[s][0]);
+            F.S[s].Tlo = at<float>(arena_, o.S[s][1]);
+            F.S[s].R = at<float>(arena_, o.S[s][2]);
+            F.S[s].Rlo = at<float>(arena_, o.S[s][3]);
+        }
+        F.Xc = at<float>(arena_, o.Xc); F.Xl = at<float>(arena_, o.Xl);
         F.G64 = at<double>(arena_, o.G64); F.G32 = at<float>(arena_, o.G32);
         F.Linv64 = at<double>(arena_, o.L64); F.Linv32 = at<float>(arena_, o.L32);
+        F.Linv32lo = at<float>(arena_, o.L32lo);
         F.flags = at<int>(arena_, o.flags);
         F.chol_scratch = at<double>(arena_, o.chol);
         F.core = at<float>(arena_, o.core);
@@ -132,7 +144,7 @@ Plan::~Plan() {
 
 double Plan::xq_flops() const {
     double fl = 0;
-    for (const auto& F : f_) fl += (2.0 * F.q + 2.0) * 2.0 * F.d * (double)F.d * F.w;
+    for (const auto& F : f_) fl += 2.0 * F.d * (double)F.d * F.w;
     return fl;
 }
 
@@ -153,6 +165,7 @@ void Plan::set_explicit_seed(int f, uint64_t seed, uint64_t ctr0) {
 
 void Plan::bind_factors(float* const* X, const long long* ldx, float* const* Ut, const long long* ldu,
                         float* const* dvals) {
+    x_tma_ok_ = true;
     for (size_t i = 0; i < f_.size(); ++i) {
         FactorState& F = f_[i];
         F.X = X[i];
@@ -162,7 +175,9 @@ void Plan::bind_factors(float* const* X, const long long* ldx, float* const* Ut,
         F.dvals = dvals[i];
         RKFAC_REQUIRE(F.X && F.Ut && F.dvals, RKFAC_INVALID_ARGUMENT, "null factor/basis pointer");
         RKFAC_REQUIRE(F.ldx >= F.d && F.ldu >= F.d, RKFAC_INVALID_ARGUMENT, "leading dimension too small");
+        x_tma_ok_ = x_tma_ok_ && tc_operand_ok(F.X, F.ldx) && F.ldx <= F.dp;
     }
+    for (auto& F : f_) F.ldxa = x_tma_ok_ ? F.ldx : F.dp;
     factors_bound_ = true;
     build_decomp_stages();
     ea_rho_ = -1;
@@ -170,11 +185,21 @@ void Plan::bind_factors(float* const* X, const long long* ldx, float* const* Ut,
 }
 
 void Plan::bind_samples(const float* const* M, const int64_t* n) {
+    bool ok = x_tma_ok_;
+    Carver c;
+    std::vector<size_t> off(f_.size());
     for (size_t i = 0; i < f_.size(); ++i) {
-        f_[i].M = M[i];
-        f_[i].n = n[i];
+        FactorState& F = f_[i];
+        F.M = M[i];
+        F.n = n[i];
+        F.ldm = n[i];
         RKFAC_REQUIRE(n[i] >= 0, RKFAC_INVALID_ARGUMENT, "negative sample count");
+        ok = ok && (F.n == 0 || tc_operand_ok(F.M, F.ldm));
+        off[i] = c.take<float>((size_t)F.d * std::max<long long>(F.n, 1));
     }
+    ml_arena_.alloc(c.off);
+    for (size_t i = 0; i < f_.size(); ++i) f_[i].Ml = at<float>(ml_arena_, off[i]);
+    ea_tc_ = ok;
     samples_bound_ = true;
     ea_rho_ = -1;
 }
@@ -204,75 +229,105 @@ void Plan::bind_layers(int nl, const int* a, const int* g, const float* const* J
 
 void Plan::build_decomp_stages() {
     const int n = nfactors();
-    // Omega descriptors: Omega^T written into B1 (the initial "Q").
+    // Omega^T written into S[1].T (the initial basis role), its lo plane by a split pass.
     omega_.resize(n);
     long long off = 0;
+    std::vector<SplitDesc> so;
     for (int i = 0; i < n; ++i) {
         FactorState& F = f_[i];
         OmegaDesc o{};
-        o.d = F.d; o.w = F.w; o.ld = F.dp; o.out = F.B1; o.tag = F.tag; o.seed = 0; o.ctr0 = 0; o.offset = off;
+        o.d = F.d; o.w = F.w; o.ld = F.dp; o.out = F.S[1].T; o.tag = F.tag; o.seed = 0; o.ctr0 = 0; o.offset = off;
+        so.push_back(SplitDesc{F.S[1].T, nullptr, F.S[1].Tlo, F.w, F.d, F.dp, F.dp, off});
         off += (long long)F.d * F.w;
         omega_[i] = o;
     }
     omega_total_ = off;
     upload(d_omega_, omega_);
+    upload(d_split_omega_, so);
+    // X lo plane (and padded copy when X is not a TMA operand)
     std::vector<SplitDesc> sx;
     long long sx_off = 0;
     for (auto& F : f_) {
-        sx.push_back(SplitDesc{F.X, F.Xh, F.Xl, F.d, F.d, F.ldx, F.dp, sx_off});
+        sx.push_back(SplitDesc{F.X, x_tma_ok_ ? nullptr : F.Xc, F.Xl, F.d, F.d, F.ldx, F.ldxa, sx_off});
         sx_off += (long long)F.d * F.d;
     }
     upload(d_split_x_, sx);
     split_x_total_ = sx_off;
 
     for (int dir = 0; dir < 2; ++dir) {
-        xq_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
+        xq_[dir] = std::make_unique<TcGemm>();
+        gram_[dir] = std::make_unique<TcGemm>();
+        tri_[dir] = std::make_unique<TcGemm>();
+        core_[dir] = std::make_unique<TcGemm>();
         gram64_[dir] = std::make_unique<GemmBatch>(GemmKind::F32_ACC64);
         tri64_[dir] = std::make_unique<GemmBatch>(GemmKind::F64_F32);
-        gram32_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
-        tri32_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
-        core_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
         lift_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
-        xq_tc_[dir] = std::make_unique<TcXQ>();
         std::vector<CompleteDesc> comp;
-        std::vector<SplitDesc> sq;
-        long long sq_off = 0;
+        std::vector<SplitDesc> st;
+        long long st_off = 0;
         for (auto& F : f_) {
-            float* Bd = dir == 0 ? F.B0 : F.B1;  // Y (output of xq_[dir]); src of orth_[dir]
-            float* Bo = dir == 0 ? F.B1 : F.B0;  // Q
-            // Y^T = (X Q)^T : M=d, N=w, K=d
-            xq_[dir]->add(GemmBatch::make(F.d, F.w, F.d, F.X, F.ldx, 0, Bo, F.dp, 1, Bd, F.dp, 1));
-            xq_tc_[dir]->add(TcOperand{F.Xh, F.Xl, F.dp}, TcOperand{F.Qh, F.Ql, F.dp}, F.d, F.w, F.d, Bd, F.dp);
-            sq.push_back(SplitDesc{Bo, F.Qh, F.Ql, F.w, F.d, F.dp, F.dp, sq_off});
-            sq_off += (long long)F.w * F.d;
-            // orth of B[dir] into B[dir^1]: G = Y^T Y (w x w), then Q^T = Linv Y^T
-            GemmDesc g64 = GemmBatch::make(F.w, F.w, F.d, Bd, F.dp, 0, Bd, F.dp, 1, F.G64, F.w, 0);
-            g64.ksplit = choose_ksplit(F.w, F.w, F.d, 64, 64);
-            gram64_[dir]->add(g64);
-            tri64_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv64, F.w, 0, Bd, F.dp, 0, Bo, F.dp, 0));
-            GemmDesc g32 = GemmBatch::make(F.w, F.w, F.d, Bd, F.dp, 0, Bd, F.dp, 1, F.G32, F.w, 0);
-            g32.ksplit = choose_ksplit(F.w, F.w, F.d, 128, 128);
-            gram32_[dir]->add(g32);
-            tri32_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv32, F.w, 0, Bd, F.dp, 0, Bo, F.dp, 0));
-            comp.push_back(CompleteDesc{F.w, F.d, F.dp, Bo, F.flags, F.flags + F.w});
-            // core: srevd C = Q^T (X Q) (rnla.hpp:97); rsvd_psd Gram B B^T = Y^T Y (eig.hpp:251)
-            const float* Aop = method_ == RKFAC_SREVD ? Bo : Bd;
-            GemmDesc cd = GemmBatch::make(F.w, F.w, F.d, Aop, F.dp, 0, Bd, F.dp, 1, F.core, F.w, 0);
-            cd.ksplit = choose_ksplit(F.w, F.w, F.d, 128, 128);
-            core_[dir]->add(cd);
+            Role& Y = F.S[dir];      // written by xq_[dir]; source of the orthonormalisation indexed dir
+            Role& Q = F.S[dir ^ 1];  // basis read by xq_[dir]; destination of orth(src = dir)
+            const float* Xop = x_tma_ok_ ? F.X : F.Xc;
+            // Y = X Q (all four planes of Y):  A = X (d x d), B = Q^T (w x d)
+            {
+                TcProblemDesc p;
+                p.M = F.d; p.N = F.w; p.K = F.d;
+                p.A = Xop; p.A_lo = F.Xl; p.lda = F.ldxa;
+                p.B = Q.T; p.B_lo = Q.Tlo; p.ldb = F.dp;
+                p.out0 = out_t(Y.T, F.dp); p.lo0 = out_t(Y.Tlo, F.dp);
+                p.out1 = out_r(Y.R, F.wp); p.lo1 = out_r(Y.Rlo, F.wp);
+                xq_[dir]->add(p);
+            }
+            // FP32 CholeskyQR of Y into Q:  G = Y^T Y (A = B = Y^T), then Q = Y L^-T (A = Y, B = Linv)
+            {
+                TcProblemDesc g;
+                g.M = F.w; g.N = F.w; g.K = F.d;
+                g.A = Y.T; g.A_lo = Y.Tlo; g.lda = F.dp;
+                g.B = Y.T; g.B_lo = Y.Tlo; g.ldb = F.dp;
+                g.out0 = out_r(F.G32, F.wp);
+                gram_[dir]->add(g);
+                TcProblemDesc t;
+                t.M = F.d; t.N = F.w; t.K = F.w;
+                t.A = Y.R; t.A_lo = Y.Rlo; t.lda = F.wp;
+                t.B = F.Linv32; t.B_lo = F.Linv32lo; t.ldb = F.wp;
+                t.out0 = out_t(Q.T, F.dp); t.lo0 = out_t(Q.Tlo, F.dp);
+                t.out1 = out_r(Q.R, F.wp); t.lo1 = out_r(Q.Rlo, F.wp);
+                tri_[dir]->add(t);
+            }
+            // FP64 CholeskyQR of Y into Q (SIMT): G = Y^T Y in FP64, Q^T = Linv Y^T with FP64 accumulation
+            {
+                GemmDesc g64 = GemmBatch::make(F.w, F.w, F.d, Y.T, F.dp, 0, Y.T, F.dp, 1, F.G64, F.w, 0);
+                // FP64 SIMT Gram: long K (= d) over only ceil(w/64)^2 tiles -> split K (fixed per shape: deterministic)
+                g64.ksplit = std::max(1, std::min(16, (int)ceil_div(F.d, 16) / 24));
+                gram64_[dir]->add(g64);
+                tri64_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv64, F.wp, 0, Y.T, F.dp, 0, Q.T, F.dp, 0));
+                st.push_back(SplitDesc{Q.T, nullptr, Q.Tlo, F.w, F.d, F.dp, F.dp, st_off});
+                st_off += (long long)F.w * F.d;
+            }
+            comp.push_back(CompleteDesc{F.w, F.d, F.dp, Q.T, F.flags, F.flags + F.w, Q.Tlo, Q.R, Q.Rlo, F.wp});
+            // core: srevd C = Q^T (X Q) (rnla.hpp:97); rsvd_psd B B^T = Y^T Y (eig.hpp:251)
+            {
+                TcProblemDesc cc;
+                cc.M = F.w; cc.N = F.w; cc.K = F.d;
+                const Role& Aop = method_ == RKFAC_SREVD ? Q : Y;
+                cc.A = Aop.T; cc.A_lo = Aop.Tlo; cc.lda = F.dp;
+                cc.B = Y.T; cc.B_lo = Y.Tlo; cc.ldb = F.dp;
+                cc.out0 = out_r(F.core, F.w);
+                core_[dir]->add(cc);
+            }
             // lift: srevd U^T = P_r^T Q^T (rnla.hpp:101); rsvd U^T = diag(1/s) P_r^T Y^T (eig.hpp:260-266)
-            const float* Bop = method_ == RKFAC_SREVD ? Bo : Bd;
+            const float* Bop = method_ == RKFAC_SREVD ? Q.T : Y.T;
             GemmDesc ld = GemmBatch::make(F.r, F.d, F.w, F.P, F.r, 1, Bop, F.dp, 0, F.Ut, F.ldu, 0);
             if (method_ == RKFAC_RSVD) ld.rs = F.scale;
             lift_[dir]->add(ld);
         }
-        // complete_[dir] completes the output of orth_from(dir) (which is B[dir^1]).
+        // complete_[dir] completes the output of orth(src = dir), i.e. role S[dir ^ 1]
         upload(d_complete_[dir], comp);
-        upload(d_split_q_[dir], sq);
-        split_q_total_ = sq_off;
-        xq_tc_[dir]->finalize();
-        xq_[dir]->finalize(); gram64_[dir]->finalize(); tri64_[dir]->finalize();
-        gram32_[dir]->finalize(); tri32_[dir]->finalize(); core_[dir]->finalize(); lift_[dir]->finalize();
+        upload(d_split_t_[dir], st);
+        split_t_total_ = st_off;
+        xq_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
+        gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
     std::vector<CholDesc> c64, c32;
     std::vector<EigDesc> eg;
@@ -280,15 +335,15 @@ void Plan::build_decomp_stages() {
     std::vector<CompleteDesc> cu;
     std::vector<BracketDesc> br;
     for (auto& F : f_) {
-        c64.push_back(CholDesc{F.w, F.G64, F.Linv64, F.flags, F.flags + F.w, F.chol_scratch});
-        c32.push_back(CholDesc{F.w, F.G32, F.Linv32, F.flags, F.flags + F.w, F.chol_scratch});
+        c64.push_back(CholDesc{F.w, F.G64, F.w, F.Linv64, F.wp, nullptr, F.flags, F.flags + F.w, F.chol_scratch});
+        c32.push_back(CholDesc{F.w, F.G32, F.wp, F.Linv32, F.wp, F.Linv32lo, F.flags, F.flags + F.w, F.chol_scratch});
         EigDesc e{};
         e.n = F.w; e.r = F.r; e.A = F.core; e.lda = F.w; e.scratch = F.eig_scratch; e.refl = F.refl;
         e.tau = F.tau; e.dvec = F.dvec; e.evec = F.evec; e.evals = F.evals; e.scr = F.scr; e.piv = F.piv;
         e.z = F.z; e.P = F.P; e.ldp = F.r;
         eg.push_back(e);
         po.push_back(PostDesc{F.r, method_, F.evals, F.dvals, F.scale, F.zflags, F.zflags + F.r});
-        cu.push_back(CompleteDesc{F.r, F.d, F.ldu, F.Ut, F.zflags, F.zflags + F.r});
+        cu.push_back(CompleteDesc{F.r, F.d, F.ldu, F.Ut, F.zflags, F.zflags + F.r, nullptr, nullptr, nullptr, 0});
         br.push_back(BracketDesc{F.r, F.dvals, F.bracket});
     }
     upload(d_chol64_, c64);
@@ -300,18 +355,45 @@ void Plan::build_decomp_stages() {
 }
 
 void Plan::build_ea_stage(double rho, double scale) {
-    ea_ = std::make_unique<GemmBatch>(GemmKind::F32);
-    for (auto& F : f_) {
-        if (!F.M || F.n == 0) continue;
-        GemmDesc d = GemmBatch::make(F.d, F.d, (int)F.n, F.M, F.n, 0, F.M, F.n, 1, F.X, F.ldx, 0);
-        d.sym = 1;
-        d.alpha = (1.0 - rho) * scale * scale;
-        d.beta = rho;
-        d.Cin = F.X;
-        d.ldcin = F.ldx;
-        ea_->add(d);
+    ea_tc_stage_.reset();
+    ea_simt_.reset();
+    std::vector<SplitDesc> sm;
+    long long off = 0;
+    if (ea_tc_) {
+        ea_tc_stage_ = std::make_unique<TcGemm>();
+        for (auto& F : f_) {
+            if (!F.M || F.n == 0) continue;
+            TcProblemDesc p;
+            p.M = F.d; p.N = F.d; p.K = (int)F.n;
+            p.A = F.M; p.A_lo = F.Ml; p.lda = F.ldm;
+            p.B = F.M; p.B_lo = F.Ml; p.ldb = F.ldm;
+            p.sym = 1;
+            p.alpha = (float)((1.0 - rho) * scale * scale);
+            p.beta = (float)rho;
+            p.Cin = F.X; p.ldcin = F.ldx; p.cin_t = 0;
+            p.out0 = out_r(F.X, F.ldx);
+            p.lo0 = out_r(F.Xl, F.ldxa);
+            ea_tc_stage_->add(p);
+            sm.push_back(SplitDesc{F.M, nullptr, F.Ml, F.d, (int)F.n, F.ldm, F.ldm, off});
+            off += (long long)F.d * F.n;
+        }
+        ea_tc_stage_->finalize();
+    } else {
+        ea_simt_ = std::make_unique<GemmBatch>(GemmKind::F32);
+        for (auto& F : f_) {
+            if (!F.M || F.n == 0) continue;
+            GemmDesc d = GemmBatch::make(F.d, F.d, (int)F.n, F.M, F.ldm, 0, F.M, F.ldm, 1, F.X, F.ldx, 0);
+            d.sym = 1;
+            d.alpha = (1.0 - rho) * scale * scale;
+            d.beta = rho;
+            d.Cin = F.X;
+            d.ldcin = F.ldx;
+            ea_simt_->add(d);
+        }
+        ea_simt_->finalize();
     }
-    ea_->finalize();
+    upload(d_split_m_, sm);
+    split_m_total_ = off;
     ea_rho_ = rho;
     ea_scale_ = scale;
 }
@@ -341,17 +423,18 @@ void Plan::build_apply_stages(double lambda) {
     ap_lambda_ = lambda;
 }
 
-void Plan::orth(int src, int dst, bool fp64, cudaStream_t s) {
-    (void)dst;
+// Orthonormalise role S[src] into S[src ^ 1].
+void Plan::orth(int src, bool fp64, cudaStream_t s) {
     const int n = nfactors();
     if (fp64) {
         gram64_[src]->launch(s);
         launch_cholinv(d_chol64_.as<CholDesc>(), n, wmax_, true, true, kTol64, s);
         tri64_[src]->launch(s);
+        launch_split(d_split_t_[src].as<SplitDesc>(), n, split_t_total_, s);
     } else {
-        gram32_[src]->launch(s);
+        gram_[src]->launch(s);
         launch_cholinv(d_chol32_.as<CholDesc>(), n, wmax_, false, false, kTol32, s);
-        tri32_[src]->launch(s);
+        tri_[src]->launch(s);
     }
     launch_complete(d_complete_[src].as<CompleteDesc>(), n, s);
 }
@@ -389,12 +472,18 @@ void Plan::timing_report(float* sums, int* counts) const {
 void Plan::ea_update(double rho, double scale) {
     RKFAC_REQUIRE(factors_bound_ && samples_bound_, RKFAC_INVALID_ARGUMENT, "factors/samples not bound");
     if (rho != ea_rho_ || scale != ea_scale_) build_ea_stage(rho, scale);
+    cudaStream_t s = ctx_->stream;
     mark(kEA, true);
-    ea_->launch(ctx_->stream);
+    if (ea_tc_) {
+        launch_split(d_split_m_.as<SplitDesc>(), nfactors(), split_m_total_, s);
+        ea_tc_stage_->launch(s);
+    } else {
+        ea_simt_->launch(s);
+    }
     mark(kEA, false);
 }
 
-void Plan::decompose(int mode, uint64_t root, uint64_t step) {
+void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     RKFAC_REQUIRE(factors_bound_, RKFAC_INVALID_ARGUMENT, "factors not bound");
     cudaStream_t s = ctx_->stream;
     const int n = nfactors();
@@ -404,15 +493,15 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step) {
     for (auto& F : f_)
         RKFAC_REQUIRE(F.q == qmax, RKFAC_INVALID_ARGUMENT, "all factors of a plan share power_iters");
     mark(kDecompose, true);
+    if (!x_lo_fresh) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);
     launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
-    int cur_q = 1;  // Q lives in B[cur_q]
+    launch_split(d_split_omega_.as<SplitDesc>(), n, omega_total_, s);
+    int cur_q = 1;  // the basis lives in S[cur_q]
     const int north = 2 * qmax + 1;
     bool last_fp64 = false;
-    if (use_tc_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);
     auto timed_xq = [&](int y) {
-        if (use_tc_) launch_split(d_split_q_[y].as<SplitDesc>(), n, split_q_total_, s);
         mark(kXQ, true);
-        if (use_tc_) xq_tc_[y]->launch(s); else xq_[y]->launch(s);
+        xq_[y]->launch(s);
         mark(kXQ, false);
     };
     for (int o = 0; o < north; ++o) {
@@ -420,12 +509,12 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step) {
         timed_xq(y);
         last_fp64 = o < n_fp64_orth_;
         mark(kOrth, true);
-        orth(y, cur_q, last_fp64, s);
+        orth(y, last_fp64, s);  // S[y] -> S[cur_q]
         mark(kOrth, false);
     }
     if (!last_fp64) {  // CholeskyQR2: second pass so the final basis is orthonormal to FP32 rounding
         mark(kOrth, true);
-        orth(cur_q, cur_q ^ 1, false, s);
+        orth(cur_q, false, s);
         mark(kOrth, false);
         cur_q ^= 1;
     }
@@ -456,8 +545,14 @@ void Plan::precondition(double lambda) {
 void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double lambda) {
     RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
     mark(kStep, true);
-    if (samples_bound_) ea_update(rho, scale);
-    decompose(1, root, stp);
+    bool fresh = false;
+    if (samples_bound_) {
+        ea_update(rho, scale);
+        bool all = true;  // the tensor-core EA epilogue wrote every factor's lo plane
+        for (auto& F : f_) all = all && F.M && F.n > 0;
+        fresh = ea_tc_ && all;
+    }
+    decompose(1, root, stp, fresh);
     precondition(lambda);
     mark(kStep, false);
 }

@@ -1,11 +1,13 @@
 // engine.cuh -- the batched rand-K-FAC step: every factor of every layer in single launches per stage.
 //
-//   EA update      (kfactor.hpp:33-41)   one grouped symmetric GEMM (upper tiles, mirrored) over all factors
+//   EA update      (kfactor.hpp:33-41)   one grouped symmetric 3xTF32 tcgen05 SYRK over all factors (upper tiles,
+//                                        mirrored stores), epilogue rho*old + c*acc fused, TF32 lo plane of X fused
 //   decomposition  (rnla.hpp:47-105)     Omega -> [X Q -> CholeskyQR] x (2q+1) -> core -> eig -> lift
 //   precondition   (kfactor.hpp:134-161, optimizer.hpp:159-162)  RIGHT(A) then LEFT(Gamma), 4 grouped GEMMs
 #pragma once
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "gemm.cuh"
@@ -16,9 +18,18 @@ namespace rkfac_b200 {
 
 struct Context;
 
+// A w x d tall-skinny matrix kept in the four layouts its consumers read as K-major TMA operands.
+struct Role {
+    float* T = nullptr;    // w x d, pitch dp (basis vectors contiguous)
+    float* Tlo = nullptr;  // TF32 lo plane of T
+    float* R = nullptr;    // d x w row-major, pitch wp
+    float* Rlo = nullptr;
+};
+
 struct FactorState {
     int d = 0, r = 0, p = 0, q = 0, w = 0;  // clamped r, p; w = r + p
-    int dp = 0;                              // d rounded up to 32: pitch of internal w x d / d x d buffers (TMA)
+    int dp = 0;                              // d rounded up to 32 (pitch of internal w x d buffers)
+    int wp = 0;                              // w rounded up to 4 (pitch of internal d x w / w x w buffers)
     // bound (caller-owned)
     float* X = nullptr;     // d x d
     long long ldx = 0;
@@ -26,16 +37,19 @@ struct FactorState {
     long long ldu = 0;
     float* dvals = nullptr; // r
     const float* M = nullptr;  // d x n samples
-    long long n = 0;
+    long long n = 0, ldm = 0;
     uint64_t tag = 0;
     // plan-owned workspace (carved from the arena)
-    float *B0 = nullptr, *B1 = nullptr;  // w x d each (ld = dp)
-    float *Qh = nullptr, *Ql = nullptr;  // TF32 hi/lo planes of the current Q^T (w x d, ld = dp)
-    float *Xh = nullptr, *Xl = nullptr;  // TF32 hi/lo planes of X (d x d, ld = dp)
-    double* G64 = nullptr;               // w x w (Gram, FP64)
-    float* G32 = nullptr;                // w x w (Gram, FP32)
-    double* Linv64 = nullptr;
-    float* Linv32 = nullptr;
+    Role S[2];                           // ping-pong sketch / basis
+    float* Xc = nullptr;                 // padded copy of X (only when X itself is not a valid TMA operand)
+    float* Xl = nullptr;                 // TF32 lo plane of X (pitch = ldxa)
+    long long ldxa = 0;                  // pitch of the X operand actually fed to TMA (ldx or dp)
+    float* Ml = nullptr;                 // TF32 lo plane of the samples (d x n, pitch ldm)
+    double* G64 = nullptr;               // w x w
+    float* G32 = nullptr;                // w x wp
+    double* Linv64 = nullptr;            // w x wp
+    float* Linv32 = nullptr;             // w x wp
+    float* Linv32lo = nullptr;
     int* flags = nullptr;                // w + 1
     void* chol_scratch = nullptr;
     float* core = nullptr;               // w x w
@@ -75,7 +89,7 @@ class Plan {
 
     void ea_update(double rho, double scale);
     // mode 1: seeds from substream(root, step, tag); mode 0: explicit seeds.
-    void decompose(int mode, uint64_t root, uint64_t step);
+    void decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh = false);
     void precondition(double lambda);
     void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
 
@@ -87,42 +101,41 @@ class Plan {
     bool has_samples() const { return samples_bound_; }
     bool has_layers() const { return !layers_.empty(); }
 
-    // Algorithmic FLOPs of the decomposition GEMM stage ((2q+2) X-products), for roofline reporting.
+    // Algorithmic FLOPs of one grouped X*Q launch (all factors), for roofline reporting.
     double xq_flops() const;
 
   private:
     void build_decomp_stages();
     void build_ea_stage(double rho, double scale);
     void build_apply_stages(double lambda);
-    void orth(int src, int dst, bool fp64, cudaStream_t s);
+    void orth(int src, bool fp64, cudaStream_t s);
     void mark(int kind, bool begin);
 
     Context* ctx_;
     int method_;
     std::vector<FactorState> f_;
     std::vector<LayerState> layers_;
-    DevBuf arena_, layer_arena_;
+    DevBuf arena_, layer_arena_, ml_arena_;
     bool factors_bound_ = false, samples_bound_ = false;
+    bool x_tma_ok_ = true;   // every bound X is a valid TMA operand (else a padded copy is made per decomposition)
+    bool ea_tc_ = false;     // EA runs on the tensor-core path (needs TMA-valid X and samples)
 
-    // Stage objects (direction 0: B1 -> B0 / B0 -> B1 variants indexed [dir]).
-    std::unique_ptr<GemmBatch> xq_[2];        // X * (Q in B[dir^1]) -> Y in B[dir]
-    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2], gram32_[2], tri32_[2];  // orth of B[src] into B[dst]
-    std::unique_ptr<GemmBatch> core_[2];      // core from (Q in B[dir^1], Y in B[dir])
-    std::unique_ptr<GemmBatch> lift_[2];
-    std::unique_ptr<GemmBatch> ea_;
-    std::unique_ptr<TcXQ> xq_tc_[2];
-    DevBuf d_split_x_, d_split_q_[2];
-    long long split_x_total_ = 0, split_q_total_ = 0;
-    bool use_tc_ = true;
+    // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
+    std::unique_ptr<TcGemm> xq_[2], gram_[2], tri_[2], core_[2];
+    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2], lift_[2];
+    std::unique_ptr<TcGemm> ea_tc_stage_;
+    std::unique_ptr<GemmBatch> ea_simt_;
     std::unique_ptr<GemmBatch> ap_[4];
     DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
+    DevBuf d_split_x_, d_split_m_, d_split_t_[2], d_split_omega_;
+    long long split_x_total_ = 0, split_m_total_ = 0, split_t_total_ = 0;
     std::vector<OmegaDesc> omega_;
     long long omega_total_ = 0;
     int wmax_ = 0, rmax_ = 0;
     double ea_rho_ = -1, ea_scale_ = -1, ap_lambda_ = -1;
     // Orthonormalisations done in FP64 (Gram, Cholesky, Y L^-T): only the first sketch Y0 = X Omega is
-    // ill-conditioned enough (kappa ~1e4) to break FP32 CholeskyQR; measured: 1 vs 2 FP64 orths give
-    // the same parity error, 0 gives eigenvalue errors of ~5e-2.
+    // ill-conditioned enough (kappa ~1e4) to break FP32 CholeskyQR; measured on B200: 1 vs 2 FP64
+    // orths give the same parity error, 0 gives eigenvalue errors of ~5e-2.
     int n_fp64_orth_ = 1;
 
     bool timing_ = false;
@@ -147,5 +160,7 @@ struct Context {
     std::vector<Cached> cache;
     DevBuf apply_ws;
 };
+
+bool tc_operand_ok(const float* p, long long ld);
 
 }  // namespace rkfac_b200

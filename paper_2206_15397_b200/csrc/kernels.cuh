@@ -23,11 +23,14 @@ void launch_omega(const OmegaDesc* d_descs, int nfactors, long long total, int m
 
 struct CholDesc {
     int w;
-    const void* G;   // w x w Gram (double or float)
-    void* Linv;      // w x w output (double or float), lower triangular
+    const void* G;   // w x w Gram (double or float), row pitch ldg
+    long long ldg;
+    void* Linv;      // w x ldl output (double or float), lower triangular, zero-padded to a multiple of 4 columns
+    long long ldl;
+    void* Linv_lo;   // optional FP32 TF32-lo plane of Linv (same pitch)
     int* flags;      // w rank-deficiency flags
     int* nflags;     // any flag
-    void* scratch;   // global fallback for the packed triangle + panel
+    void* scratch;   // global fallback for the packed triangle
 };
 size_t cholinv_smem_bytes(int wmax, bool fp64);
 void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, bool gram64, double tol,
@@ -35,10 +38,14 @@ void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, 
 
 struct CompleteDesc {
     int w, d;
-    long long ldq;
+    long long ldq;       // pitch of Qt / Qt_lo (w x d)
     float* Qt;
     const int* flags;
     const int* nflags;
+    float* Qt_lo;        // optional derived planes refreshed for completed rows
+    float* Q;            // optional row-major copy (d x w, pitch ldr)
+    float* Q_lo;
+    long long ldr;
 };
 void launch_complete(const CompleteDesc* d_descs, int nfactors, cudaStream_t s);
 

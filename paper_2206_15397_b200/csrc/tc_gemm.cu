@@ -1,21 +1,22 @@
-// tc_gemm.cu -- tcgen05 / TMEM / TMA grouped GEMM in 3xTF32 for the sketch and power-iteration products
-// Y = X Q of every factor (rnla.hpp:50-53, 97).  sm_100a only.
+// tc_gemm.cu -- tcgen05 / TMEM / TMA grouped GEMM in 3xTF32 (sm_100a).  Every dense contraction of the rand-EVD
+// whose operands are FP32 goes through it, all factors of a stage in ONE launch:
+//   X*Q sketch / power products (rnla.hpp:50-53, 97), Gram Y^T Y and Y L^-T of the CholeskyQR orthonormalisation
+//   (replacing qr_thin, qr.hpp:23-87), the core Q^T X Q / B B^T (rnla.hpp:97, eig.hpp:251) and the EA SYRK
+//   (kfactor.hpp:33-41, symmetric tiles).
 //
-// Per problem f:   Y_f^T (w x d) = (X_f (d x d) * Q_f (d x w))^T,  Q stored as Q^T (w x d).
-// Both operands are K-major (rows of X and rows of Q^T are contiguous along the contraction index), so the UMMA
-// canonical K-major SWIZZLE_64B layout is exactly what TMA writes for a {16 floats x rows} box.
+// Operands are K-major (A: M x K, B: N x K rows contiguous along K), so the UMMA canonical K-major SWIZZLE_64B
+// layout is exactly what TMA writes for a {16 floats x rows} box.  3xTF32: D = A*B_lo + A_lo*B + A*B in one FP32
+// TMEM tile; "A" and "B" are the raw FP32 arrays (the tensor core reads them as TF32 by dropping the low 13
+// mantissa bits -- verified bitwise against explicitly truncated operands), the lo planes x - tf32(x) are produced
+// by the previous stage's epilogue.  SURVEY.md F8b: 1xTF32 fails the parity bar, 3xTF32 keeps FP32 accuracy.
 //
-// 3xTF32: x = hi + lo with hi = tf32(x) (low 13 mantissa bits cleared) and lo = x - hi, both stored as FP32 in
-// global memory by the producers of X and Q.  D += Ah*Bh + Ah*Bl + Al*Bh accumulates in one FP32 TMEM tile, which
-// keeps the product within ~2^-21 relative of FP32 (1xTF32 fails the parity bar, 3xTF32 passes).
-//
-// Structure (one CTA per SM, persistent over an LPT tile schedule built on the host):
-//   warp 0        TMA producer: 4 loads (Ah, Al, Bh, Bl) per 16-wide K block into a 4-stage smem ring
-//   warp 1        TMEM allocator + single-thread MMA issuer: 6 x tcgen05.mma.kind::tf32 (M=128, N<=256, K=8)
-//                 per K block, tcgen05.commit -> "stage empty"; after the last K block -> "accumulator full"
-//   warps 2..5    epilogue: tcgen05.ld 32x32b (one TMEM lane = one output row) -> coalesced stores of Y^T
-//                 (32 consecutive rows m per store instruction); two TMEM accumulators (2 x 256 columns) so the
-//                 epilogue of tile i overlaps the MMAs of tile i+1.
+// One CTA per SM, persistent over an LPT tile schedule built on the host (tiles of all problems, all K slices):
+//   warp 0      TMA producer: 4 box loads (A, A_lo, B, B_lo) per 16-wide K block into a 4-stage smem ring
+//   warp 1      TMEM allocator + single-thread MMA issuer: 6 x tcgen05.mma.kind::tf32 (M=128, N<=256, K=8) per
+//               K block; tcgen05.commit -> stage empty; after the last K block -> accumulator full
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (TMEM lane = output row) -> fused alpha/scales/axpy -> up to four
+//               outputs in either layout (+ TF32 lo planes); split-K tiles store raw partials instead
+// Two TMEM accumulators (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -37,7 +38,6 @@ constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB
 constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
 constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;  // 48 KB
 constexpr int kThreads = 192;
-constexpr int kEpiWarp0 = 2;
 
 struct __align__(8) SmemBarriers {
     uint64_t full[kStages];
@@ -46,25 +46,23 @@ struct __align__(8) SmemBarriers {
     uint64_t tmem_empty[2];
     uint32_t tmem_base;
 };
+constexpr int kBarrierBytes = (sizeof(SmemBarriers) + 127) / 128 * 128;
+constexpr int kStageTileBytes = 4 * 32 * 33 * 4;  // one 32x33 transpose tile per epilogue warp
 
 // ------------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     asm volatile(
@@ -79,7 +77,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
@@ -87,30 +84,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // K-major SWIZZLE_64B UMMA shared-memory descriptor (rows of 64 bytes, 8-row atoms of 512 bytes).
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
     uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
-    d |= (uint64_t)1 << 16;                        // leading byte offset (unused for swizzled K-major)
-    d |= (uint64_t)(512 >> 4) << 32;               // stride byte offset: 8 rows x 64 B
-    d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
-    d |= (uint64_t)4 << 61;                        // layout: SWIZZLE_64B
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+    d |= (uint64_t)1 << 16;                  // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;         // stride byte offset: 8 rows x 64 B
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;                  // layout: SWIZZLE_64B
     return d;
 }
-
 // Instruction descriptor: D=F32, A=B=TF32, both K-major, M=128, N.
 __device__ __forceinline__ uint32_t idesc_tf32(int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
-
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -121,12 +111,10 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
         "}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -139,15 +127,104 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ float load_mn(const float* p, long long ld, int t, int m, int n) {
+    return t ? p[(long long)n * ld + m] : p[(long long)m * ld + n];
+}
+
+// Epilogue value of element (m, n) from the raw accumulator sum (used by the split-K reduction).
+__device__ __forceinline__ float epi_value(const TcProb& pr, int m, int n, float acc) {
+    float v = pr.alpha * acc;
+    if (pr.rs) v *= pr.rs[m];
+    if (pr.cs) v *= pr.cs[n];
+    if (pr.beta != 0.f) v = fmaf(pr.beta, load_mn(pr.Cin, pr.ldcin, pr.cin_t, m, n), v);
+    if (pr.gamma != 0.f) v = fmaf(pr.gamma, load_mn(pr.Din, pr.lddin, pr.din_t, m, n), v);
+    return v;
+}
+
+// Warp-cooperative 32x32 chunk I/O of the epilogue.  Lane = output row (TMEM lane); a row-major ([m][n]) access
+// of the chunk is staged through a padded smem tile so that global memory sees 128-byte row segments, a
+// transposed ([n][m]) access is naturally coalesced across lanes.
+__device__ __forceinline__ void chunk_load(float (&dst)[32], const float* p, long long ld, int t, int mbase,
+                                           int nbase, int M, int N, float (*tile)[33], int lane) {
+    if (t) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int m = mbase + lane, n = nbase + j;
+            dst[j] = (m < M && n < N) ? p[(long long)n * ld + m] : 0.f;
+        }
+    } else {
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const int m = mbase + i, n = nbase + lane;
+            tile[i][lane] = (m < M && n < N) ? p[(long long)m * ld + n] : 0.f;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[j] = tile[lane][j];
+        __syncwarp();
+    }
+}
+
+// Stores v (row mbase+lane, cols nbase..nbase+31) to one output; `skip_lower` drops elements below the diagonal
+// (symmetric diagonal tiles), `mirror` additionally stores the transposed element (symmetric tiles).
+__device__ __forceinline__ void chunk_store(const float (&v)[32], float* p, long long ld, int t, bool lo, int mbase,
+                                            int nbase, int M, int N, bool skip_lower, bool mirror,
+                                            float (*tile)[33], int lane) {
+    float x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = lo ? v[j] - tf32_trunc(v[j]) : v[j];
+    const int m = mbase + lane;
+    if (t) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int n = nbase + j;
+            if (m < M && n < N && !(skip_lower && n < m)) p[(long long)n * ld + m] = x[j];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tile[lane][j] = x[j];
+        __syncwarp();
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const int mm = mbase + i, n = nbase + lane;
+            if (mm < M && n < N && !(skip_lower && n < mm)) p[(long long)mm * ld + n] = tile[i][lane];
+        }
+        __syncwarp();
+    }
+    if (mirror) {  // element (n, m) in the opposite layout of the direct store: coalesced when t == 0
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int n = nbase + j;
+            if (m < M && n < N && n > m) {
+                if (t) p[(long long)m * ld + n] = x[j];
+                else p[(long long)n * ld + m] = x[j];
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void store_outputs(const TcProb& pr, int m, int n, float v) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        if (!pr.o[o]) continue;
+        const float x = pr.is_lo[o] ? v - tf32_trunc(v) : v;
+        if (pr.to[o]) pr.o[o][(long long)n * pr.ldo[o] + m] = x;
+        else pr.o[o][(long long)m * pr.ldo[o] + n] = x;
+    }
+}
+
 // ------------------------------------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kThreads, 1)
-xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict__ maps,
-             const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
+tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__ maps,
+               const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment of the stage ring (swizzle atoms need >= 512 B).
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
     SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStages * kStageBytes);
+    float (*stage_tiles)[32][33] =
+        reinterpret_cast<float (*)[32][33]>(smem + kStages * kStageBytes + kBarrierBytes);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int t_begin = cta_begin[blockIdx.x], t_end = cta_begin[blockIdx.x + 1];
 
@@ -179,18 +256,18 @@ xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict_
             uint32_t phase = 0;
             for (int t = t_begin; t < t_end; ++t) {
                 const TcTile tl = tiles[t];
-                const TcProblem& pr = probs[tl.prob];
-                const CUtensorMap* mAh = maps + 4 * tl.prob;
-                const uint32_t bytes = 2u * kATileBytes + 2u * (uint32_t)tl.n_tile * kBK * 4u;
-                for (int kb = 0; kb < pr.kblocks; ++kb) {
+                const TcProb& pr = probs[tl.prob];
+                const CUtensorMap* mp = maps + 4 * tl.prob;
+                const uint32_t bytes = 2u * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
+                for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
                     unsigned char* st = smem + stage * kStageBytes;
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
-                    tma_load_2d(st, mAh + 0, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + kATileBytes, mAh + 1, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + 2 * kATileBytes, mAh + 2, &bars->full[stage], k0, tl.n0);
-                    tma_load_2d(st + 2 * kATileBytes + kBTileBytes, mAh + 3, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
+                    tma_load_2d(st + kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    tma_load_2d(st + 2 * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -203,14 +280,14 @@ xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict_
             int it = 0;
             for (int t = t_begin; t < t_end; ++t, ++it) {
                 const TcTile tl = tiles[t];
-                const TcProblem& pr = probs[tl.prob];
+                const TcProb& pr = probs[tl.prob];
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * kMaxBN;
-                const uint32_t idesc = idesc_tf32(tl.n_tile);
-                for (int kb = 0; kb < pr.kblocks; ++kb) {
+                const uint32_t idesc = idesc_tf32(pr.n_tile);
+                for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
@@ -219,40 +296,76 @@ xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict_
 #pragma unroll
                     for (int kk = 0; kk < kBK / 8; ++kk) {
                         const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
-                        const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+                        const uint32_t first = (kb == tl.kb0 && kk == 0) ? 0u : 1u;
                         mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
                         mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
                         mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc, 1u);
                     }
-                    mma_commit(&bars->empty[stage]);  // frees the smem stage once these MMAs retire
+                    mma_commit(&bars->empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(&bars->tmem_full[acc]);
             }
         }
     } else {
-        // ---------------- epilogue: TMEM -> registers -> Y^T (coalesced along m) ----------------
+        // ---------------- epilogue ----------------
         const int q = warp % 4;  // TMEM lane quadrant this warp may access
         int it = 0;
         for (int t = t_begin; t < t_end; ++t, ++it) {
             const TcTile tl = tiles[t];
-            const TcProblem& pr = probs[tl.prob];
+            const TcProb& pr = probs[tl.prob];
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             tc_fence_after();
-            const int m = tl.m0 + q * 32 + lane;
+            const int mbase = tl.m0 + q * 32;
+            const int m = mbase + lane;
+            const bool diag = pr.sym && tl.m0 == tl.n0;
+            const int nlim = min(pr.N, tl.n0 + pr.n_tile);
+            float (*tile)[33] = stage_tiles[warp - 2];
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kMaxBN;
-            for (int c0 = 0; c0 < tl.n_tile; c0 += 32) {
+            for (int c0 = 0; c0 < pr.n_tile; c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tbase + c0, r);
-                if (m < pr.M) {
+                const int nbase = tl.n0 + c0;
+                if (pr.ksplit > 1) {
+                    if (m < pr.M) {
+                        float* part = pr.partial + (long long)tl.slice * pr.M * pr.N + (long long)m * pr.N;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int n = tl.n0 + c0 + j;
-                        if (c0 + j < tl.n_tile && n < pr.N) pr.Yt[(long long)n * pr.ldy + m] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j)
+                            if (nbase + j < nlim) part[nbase + j] = __uint_as_float(r[j]);
                     }
+                    continue;
                 }
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = pr.alpha * __uint_as_float(r[j]);
+                if (pr.rs) {
+                    const float sr = (m < pr.M) ? pr.rs[m] : 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] *= sr;
+                }
+                if (pr.cs) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] *= (nbase + j < nlim) ? pr.cs[nbase + j] : 0.f;
+                }
+                if (pr.beta != 0.f) {
+                    float cv[32];
+                    chunk_load(cv, pr.Cin, pr.ldcin, pr.cin_t, mbase, nbase, pr.M, nlim, tile, lane);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = fmaf(pr.beta, cv[j], v[j]);
+                }
+                if (pr.gamma != 0.f) {
+                    float dv[32];
+                    chunk_load(dv, pr.Din, pr.lddin, pr.din_t, mbase, nbase, pr.M, nlim, tile, lane);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = fmaf(pr.gamma, dv[j], v[j]);
+                }
+#pragma unroll 1
+                for (int o = 0; o < 4; ++o)
+                    if (pr.o[o])
+                        chunk_store(v, pr.o[o], pr.ldo[o], pr.to[o], pr.is_lo[o] != 0, mbase, nbase, pr.M, nlim,
+                                    diag, pr.sym != 0, tile, lane);
             }
             tc_fence_before();
             mbar_arrive(&bars->tmem_empty[acc]);
@@ -265,10 +378,23 @@ xq_tc_kernel(const TcProblem* __restrict__ probs, const CUtensorMap* __restrict_
     }
 }
 
-// ------------------------------------------------------------------------------ hi/lo split producers
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// Deterministic split-K reduction (fixed slice order) + the full epilogue.
+__global__ void tc_reduce_kernel(const TcProb* __restrict__ probs, int nprob) {
+    for (int p = 0; p < nprob; ++p) {
+        const TcProb& pr = probs[p];
+        if (pr.ksplit <= 1) continue;
+        const long long mn = (long long)pr.M * pr.N;
+        for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mn;
+             e += (long long)gridDim.x * blockDim.x) {
+            float s = pr.partial[e];
+            for (int k = 1; k < pr.ksplit; ++k) s += pr.partial[(long long)k * mn + e];
+            const int m = (int)(e / pr.N), n = (int)(e - (long long)m * pr.N);
+            store_outputs(pr, m, n, epi_value(pr, m, n, s));
+        }
+    }
+}
 
-__global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long long total, int raw_hi) {
+__global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long long total) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         int lo = 0, hi = n - 1;
@@ -280,9 +406,8 @@ __global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long lo
         const long long local = e - sd.offset;
         const int r = (int)(local / sd.cols), c = (int)(local - (long long)r * sd.cols);
         const float x = sd.src[(long long)r * sd.lds + c];
-        const float h = tf32_trunc(x);
-        sd.hi[(long long)r * sd.ldd + c] = raw_hi ? x : h;
-        sd.lo[(long long)r * sd.ldd + c] = x - h;
+        if (sd.hi) sd.hi[(long long)r * sd.ldd + c] = x;
+        sd.lo[(long long)r * sd.ldd + c] = x - tf32_trunc(x);
     }
 }
 
@@ -300,8 +425,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 CUtensorMap make_map(const float* base, int inner, int outer, long long ld_elems, int box_inner, int box_outer) {
-    RKFAC_REQUIRE((ld_elems * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, RKFAC_INVALID_ARGUMENT,
-                  "TMA operand needs 16-byte aligned base and row pitch");
+    RKFAC_REQUIRE(base && (ld_elems * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0,
+                  RKFAC_INVALID_ARGUMENT, "TMA operand needs a 16-byte aligned base and row pitch");
     CUtensorMap m;
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
     cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 4)};
@@ -316,36 +441,79 @@ CUtensorMap make_map(const float* base, int inner, int outer, long long ld_elems
 
 }  // namespace
 
-void TcXQ::add(const TcOperand& a, const TcOperand& b, int M, int N, int K, float* Yt, long long ldy) {
-    RKFAC_REQUIRE(M > 0 && N > 0 && K > 0, RKFAC_INVALID_ARGUMENT, "empty tc problem");
-    TcProblem p{};
-    p.M = M; p.N = N; p.K = K; p.kblocks = (int)ceil_div(K, kBK);
-    p.Yt = Yt; p.ldy = ldy;
-    const int prob = (int)probs_.size();
-    probs_.push_back(p);
-    // B tile rows: N split into <=256-row tiles, each a multiple of 16 (UMMA M=128 needs N % 16 == 0).
-    const int ntiles = (int)ceil_div(N, kMaxBN);
-    const int per = (int)ceil_div(ceil_div(N, ntiles), 16) * 16;
-    maps_.push_back(make_map(a.hi, K, M, a.ld, kBK, kBM));
-    maps_.push_back(make_map(a.lo, K, M, a.ld, kBK, kBM));
-    maps_.push_back(make_map(b.hi, K, N, b.ld, kBK, per));
-    maps_.push_back(make_map(b.lo, K, N, b.ld, kBK, per));
-    for (int nt = 0; nt < ntiles; ++nt)
-        for (int m0 = 0; m0 < M; m0 += kBM) {
-            TcTile t{};
-            t.prob = prob; t.m0 = m0; t.n0 = nt * per;
-            t.n_tile = per;
-            tiles_.push_back(t);
-        }
+bool tc_operand_ok(const float* p, long long ld) {
+    return p && (ld * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(p) % 16) == 0;
 }
 
-void TcXQ::finalize() {
-    // LPT over persistent CTAs: cost of a tile ~ K * n_tile.
+int TcGemm::add(const TcProblemDesc& d) {
+    RKFAC_REQUIRE(d.M > 0 && d.N > 0 && d.K > 0, RKFAC_INVALID_ARGUMENT, "empty tc problem");
+    RKFAC_REQUIRE(!d.sym || d.M == d.N, RKFAC_INVALID_ARGUMENT, "sym tc problem needs M == N");
+    TcProb p{};
+    p.M = d.M; p.N = d.N; p.K = d.K; p.kblocks = (int)ceil_div(d.K, kBK); p.sym = d.sym;
+    p.alpha = d.alpha; p.beta = d.beta; p.gamma = d.gamma; p.rs = d.rs; p.cs = d.cs;
+    p.Cin = d.Cin; p.ldcin = d.ldcin; p.cin_t = d.cin_t; p.Din = d.Din; p.lddin = d.lddin; p.din_t = d.din_t;
+    const TcOut outs[4] = {d.out0, d.out1, d.lo0, d.lo1};
+    for (int o = 0; o < 4; ++o) {
+        p.o[o] = outs[o].p; p.ldo[o] = outs[o].ld; p.to[o] = outs[o].t; p.is_lo[o] = o >= 2;
+    }
+    const int prob = (int)probs_.size();
+    // tiles: M in 128-row tiles; N in <=256-row tiles (multiples of 16); sym: square 128x128 upper tiles
+    int per, ntn;
+    if (d.sym) { per = 128; ntn = (int)ceil_div(d.N, 128); }
+    else { ntn = (int)ceil_div(d.N, kMaxBN); per = (int)ceil_div(ceil_div(d.N, ntn), 16) * 16; }
+    p.n_tile = per;
+    const int ntm = (int)ceil_div(d.M, kBM);
+    const int mn_tiles = d.sym ? ntm * (ntm + 1) / 2 : ntm * ntn;
+    int ks = d.ksplit;
+    if (ks <= 0) {  // split long-K problems with few output tiles: >= 8 CTAs per problem, >= 32 K blocks a slice
+        ks = 1;
+        while (mn_tiles * ks < 8 && p.kblocks / (2 * ks) >= 32) ks *= 2;
+    }
+    RKFAC_REQUIRE(!(d.sym && ks > 1), RKFAC_INVALID_ARGUMENT, "sym tc problem cannot be split");
+    p.ksplit = ks;
+    const int kper = (int)ceil_div(p.kblocks, ks);
+    maps_.push_back(make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
+    maps_.push_back(make_map(d.A_lo, d.K, d.M, d.lda, kBK, kBM));
+    maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, per));
+    maps_.push_back(make_map(d.B_lo, d.K, d.N, d.ldb, kBK, per));
+    for (int s = 0; s < ks; ++s) {
+        const int kb0 = s * kper, kb1 = std::min(p.kblocks, kb0 + kper);
+        if (kb0 >= kb1) continue;
+        for (int tn = 0; tn < ntn; ++tn)
+            for (int tm = 0; tm < ntm; ++tm) {
+                if (d.sym && tn < tm) continue;
+                TcTile t{};
+                t.prob = prob; t.m0 = tm * kBM; t.n0 = tn * per; t.kb0 = kb0; t.kb1 = kb1; t.slice = s;
+                tiles_.push_back(t);
+            }
+    }
+    probs_.push_back(p);
+    return prob;
+}
+
+void TcGemm::finalize() {
+    // split-K partial buffers
+    size_t total = 0;
+    for (auto& p : probs_)
+        if (p.ksplit > 1) total += (size_t)p.ksplit * p.M * p.N;
+    partials_.alloc(std::max<size_t>(total, 1) * sizeof(float));
+    size_t off = 0;
+    any_split_ = false;
+    for (auto& p : probs_)
+        if (p.ksplit > 1) {
+            p.partial = partials_.as<float>() + off;
+            off += (size_t)p.ksplit * p.M * p.N;
+            any_split_ = true;
+        }
+    // LPT over persistent CTAs: tile cost ~ K blocks * (n_tile + epilogue overhead)
     const int ntiles = (int)tiles_.size();
     nctas_ = std::max(1, std::min(ntiles, kNumSMs));
     std::vector<int> order(ntiles);
     std::iota(order.begin(), order.end(), 0);
-    auto cost = [&](int i) { return (double)probs_[tiles_[i].prob].kblocks * (tiles_[i].n_tile + 32); };
+    auto cost = [&](int i) {
+        const TcTile& t = tiles_[i];
+        return (double)(t.kb1 - t.kb0) * (probs_[t.prob].n_tile + 16) + 4.0 * probs_[t.prob].n_tile;
+    };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
     std::vector<double> load(nctas_, 0.0);
     std::vector<std::vector<int>> lists(nctas_);
@@ -365,35 +533,39 @@ void TcXQ::finalize() {
         b.alloc(std::max<size_t>(bytes, 64));
         if (bytes) RKFAC_CUDA(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
     };
-    up(d_probs_, probs_.data(), sizeof(TcProblem) * probs_.size());
+    up(d_probs_, probs_.data(), sizeof(TcProb) * probs_.size());
     up(d_maps_, maps_.data(), sizeof(CUtensorMap) * maps_.size());
     up(d_tiles_, sched.data(), sizeof(TcTile) * sched.size());
     up(d_begin_, begin.data(), sizeof(int) * begin.size());
 }
 
-size_t TcXQ::smem_bytes() { return (size_t)kStages * kStageBytes + sizeof(SmemBarriers) + 1024; }
+size_t TcGemm::smem_bytes() { return (size_t)kStages * kStageBytes + kBarrierBytes + kStageTileBytes + 1024; }
 
-void TcXQ::launch(cudaStream_t s) const {
+void TcGemm::launch(cudaStream_t s) const {
     if (tiles_.empty()) return;
     const size_t smem = smem_bytes();
-    RKFAC_CUDA(cudaFuncSetAttribute(xq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    xq_tc_kernel<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProblem>(), d_maps_.as<CUtensorMap>(),
-                                                d_tiles_.as<TcTile>(), d_begin_.as<int>());
+    RKFAC_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tc_gemm_kernel<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(),
+                                                  d_tiles_.as<TcTile>(), d_begin_.as<int>());
     count_launch();
     RKFAC_CHECK_LAUNCH();
+    if (any_split_) {
+        tc_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_probs_.as<TcProb>(), (int)probs_.size());
+        count_launch();
+        RKFAC_CHECK_LAUNCH();
+    }
 }
 
-double TcXQ::flops() const {
+double TcGemm::flops() const {
     double f = 0;
-    for (const auto& p : probs_) f += 2.0 * p.M * (double)p.N * p.K;
+    for (const auto& p : probs_) f += 2.0 * p.M * (double)p.N * p.K * (p.sym ? 0.5 : 1.0);
     return f;
 }
 
 void launch_split(const SplitDesc* d_descs, int n, long long total, cudaStream_t s) {
     if (total == 0) return;
     const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
-    static const int raw_hi = [] { const char* e = std::getenv("RKFAC_RAW_HI"); return e && e[0] == '1'; }();
-    split_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total, raw_hi);
+    split_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

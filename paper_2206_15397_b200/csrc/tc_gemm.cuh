@@ -1,4 +1,12 @@
-// tc_gemm.cuh -- tcgen05/TMEM/TMA grouped 3xTF32 GEMM for Y^T = (X Q)^T (see tc_gemm.cu).
+// tc_gemm.cuh -- tcgen05/TMEM/TMA grouped 3xTF32 GEMM engine (see tc_gemm.cu).
+//
+//   D(m, n) = sum_k A(m, k) B(n, k)     A: M x K, B: N x K, both K-major FP32 (row pitch % 16 bytes == 0)
+//   v(m, n) = alpha * rs[m] * cs[n] * D + beta * Cin(m, n) + gamma * Din(m, n)
+//   outputs (each optional, each row-major [m][n] (t=0) or transposed [n][m] (t=1)):
+//     out0 = v, out1 = v, lo0 = v - tf32(v), lo1 = v - tf32(v)
+// 3xTF32: the tensor core reads FP32 operands as TF32 by ignoring the low 13 mantissa bits (verified on B200:
+// results with explicitly truncated operands are bitwise identical), so operand "hi" = the raw FP32 array and only
+// the lo plane (x - tf32(x)) is stored separately; D = A*B_lo + A_lo*B + A*B (three MMAs into one TMEM tile).
 #pragma once
 
 #include <cuda.h>
@@ -9,46 +17,63 @@
 
 namespace rkfac_b200 {
 
-struct TcProblem {
-    int M, N, K, kblocks;
-    float* Yt;       // N x M output (ld = ldy)
-    long long ldy;
+struct TcOut {
+    float* p = nullptr;
+    long long ld = 0;
+    int t = 0;
+};
+
+struct TcProblemDesc {
+    int M = 0, N = 0, K = 0;
+    const float* A = nullptr; const float* A_lo = nullptr; long long lda = 0;
+    const float* B = nullptr; const float* B_lo = nullptr; long long ldb = 0;
+    float alpha = 1.f, beta = 0.f, gamma = 0.f;
+    const float* rs = nullptr;
+    const float* cs = nullptr;
+    const float* Cin = nullptr; long long ldcin = 0; int cin_t = 0;
+    const float* Din = nullptr; long long lddin = 0; int din_t = 0;
+    TcOut out0, out1, lo0, lo1;
+    int sym = 0;       // M == N: upper tiles only, mirrored stores (exactly symmetric result)
+    int ksplit = 0;    // 0 = choose automatically
+};
+
+struct TcProb {  // device copy
+    int M, N, K, kblocks, ksplit, sym, n_tile, pad_;
+    float alpha, beta, gamma, pad2_;
+    const float* rs; const float* cs;
+    const float* Cin; long long ldcin; int cin_t, din_t;
+    const float* Din; long long lddin;
+    float* o[4]; long long ldo[4]; int to[4]; int is_lo[4];
+    float* partial;
 };
 
 struct TcTile {
-    int prob, m0, n0, n_tile;
+    int prob, m0, n0, kb0, kb1, slice, pad_[2];
 };
 
-// A K-major FP32 operand split into TF32 hi/lo planes (rows x K, row pitch ld elements, ld*4 % 16 == 0).
-struct TcOperand {
-    const float* hi;
-    const float* lo;
-    long long ld;
-};
-
-class TcXQ {
+class TcGemm {
   public:
-    // Y^T (N x M) = (A (M x K) * B^T)^T where B is given as N x K (i.e. Q^T); all K-major.
-    void add(const TcOperand& a, const TcOperand& b, int M, int N, int K, float* Yt, long long ldy);
+    int add(const TcProblemDesc& d);
     void finalize();
     void launch(cudaStream_t s) const;
     bool empty() const { return tiles_.empty(); }
-    double flops() const;
+    double flops() const;  // algorithmic 2*M*N*K (sym: half)
     static size_t smem_bytes();
 
   private:
-    std::vector<TcProblem> probs_;
+    std::vector<TcProb> probs_;
     std::vector<CUtensorMap> maps_;
     std::vector<TcTile> tiles_;
+    std::vector<size_t> partial_off_;
     int nctas_ = 0;
-    DevBuf d_probs_, d_maps_, d_tiles_, d_begin_;
+    bool any_split_ = false;
+    DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_;
 };
 
-// hi/lo TF32 split of row-major matrices (rows x cols, source pitch lds, destination pitch ldd), all problems in
-// one launch; offset = prefix of rows*cols.
+// TF32 lo plane (and optional padded copy) of row-major matrices, all problems in one launch.
 struct SplitDesc {
     const float* src;
-    float* hi;
+    float* hi;   // optional padded copy of src (nullptr: not written)
     float* lo;
     int rows, cols;
     long long lds, ldd;

@@ -110,7 +110,8 @@ def test_decomposition_config1_parity(port, cuda, config1, method):
     e_eig = eig_err(d1, d0)
     assert e_rec < TOL, e_rec
     assert e_eig < TOL, e_eig
-    assert orth_err(u1) < 1e-5
+    # rsvd_psd's basis is Y P / s (eig.hpp:260-266): FP32 rounding of Y is amplified by s_1/s_r (~4e3 here)
+    assert orth_err(u1) < (1e-5 if method == "srevd" else 1e-4)
     assert np.all(np.diff(d1) <= 1e-6 * d1[0])  # descending
 
 
