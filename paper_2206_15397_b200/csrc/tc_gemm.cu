@@ -47,7 +47,7 @@ struct __align__(8) SmemBarriers {
     uint32_t tmem_base;
 };
 constexpr int kBarrierBytes = (sizeof(SmemBarriers) + 127) / 128 * 128;
-constexpr int kStageTileBytes = 4 * 32 * 33 * 4;  // one 32x33 transpose tile per epilogue warp
+constexpr int kStageTileBytes = 4 * 32 * 36 * 4;  // one 32x36 transpose tile per epilogue warp
 
 // ------------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,7 +69,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred P1;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n"
         "@P1 bra DONE;\n"
         "bra LAB_WAIT;\n"
         "DONE:\n"
@@ -146,8 +146,43 @@ __device__ __forceinline__ float epi_value(const TcProb& pr, int m, int n, float
 // Warp-cooperative 32x32 chunk I/O of the epilogue.  Lane = output row (TMEM lane); a row-major ([m][n]) access
 // of the chunk is staged through a padded smem tile so that global memory sees 128-byte row segments, a
 // transposed ([n][m]) access is naturally coalesced across lanes.
+// Row-major 32x32 chunk accesses are done as 8 x 128-bit accesses per lane (lane covers row 4*i + lane/8,
+// columns 4*(lane%8)..+3), all issued back to back, and transposed through a [32][36] smem tile.
+constexpr int kTP = 36;  // staging tile pitch (floats): 16-byte aligned rows
+
+__device__ __forceinline__ void rm_issue(float4 (&pre)[8], const float* p, long long ld, int mbase, int nbase, int M,
+                                         int N, int lane) {
+    const int c = (lane & 7) * 4;
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) | (uintptr_t)(ld * 4)) & 15) == 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = mbase + i * 4 + (lane >> 3), n = nbase + c;
+        if (vec && m < M && n + 3 < N) {
+            pre[i] = *reinterpret_cast<const float4*>(p + (long long)m * ld + n);
+        } else {
+            float e[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] = (m < M && n + u < N) ? p[(long long)m * ld + n + u] : 0.f;
+            pre[i] = make_float4(e[0], e[1], e[2], e[3]);
+        }
+    }
+}
+
+__device__ __forceinline__ void rm_finish(float (&dst)[32], const float4 (&pre)[8], float (*tile)[kTP], int lane) {
+    const int c = (lane & 7) * 4;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) *reinterpret_cast<float4*>(&tile[i * 4 + (lane >> 3)][c]) = pre[i];
+    __syncwarp();
+#pragma unroll
+    for (int j4 = 0; j4 < 32; j4 += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(&tile[lane][j4]);
+        dst[j4] = q.x; dst[j4 + 1] = q.y; dst[j4 + 2] = q.z; dst[j4 + 3] = q.w;
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ void chunk_load(float (&dst)[32], const float* p, long long ld, int t, int mbase,
-                                           int nbase, int M, int N, float (*tile)[33], int lane) {
+                                           int nbase, int M, int N, float (*tile)[kTP], int lane) {
     if (t) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -155,41 +190,57 @@ __device__ __forceinline__ void chunk_load(float (&dst)[32], const float* p, lon
             dst[j] = (m < M && n < N) ? p[(long long)n * ld + m] : 0.f;
         }
     } else {
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-            const int m = mbase + i, n = nbase + lane;
-            tile[i][lane] = (m < M && n < N) ? p[(long long)m * ld + n] : 0.f;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) dst[j] = tile[lane][j];
-        __syncwarp();
+        float4 pre[8];
+        rm_issue(pre, p, ld, mbase, nbase, M, N, lane);
+        rm_finish(dst, pre, tile, lane);
     }
 }
 
 // Stores v (row mbase+lane, cols nbase..nbase+31) to one output; `skip_lower` drops elements below the diagonal
 // (symmetric diagonal tiles), `mirror` additionally stores the transposed element (symmetric tiles).
+__device__ __forceinline__ float lo_or(float x, bool lo) { return lo ? x - tf32_trunc(x) : x; }
+
+// Scalar store of one element to every output (split-K reduction path).
+__device__ __forceinline__ void store_outputs(const TcProb& pr, int m, int n, float v) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        if (!pr.o[o]) continue;
+        const float x = lo_or(v, pr.is_lo[o] != 0);
+        if (pr.to[o]) pr.o[o][(long long)n * pr.ldo[o] + m] = x;
+        else pr.o[o][(long long)m * pr.ldo[o] + n] = x;
+    }
+}
+
 __device__ __forceinline__ void chunk_store(const float (&v)[32], float* p, long long ld, int t, bool lo, int mbase,
                                             int nbase, int M, int N, bool skip_lower, bool mirror,
-                                            float (*tile)[33], int lane) {
-    float x[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = lo ? v[j] - tf32_trunc(v[j]) : v[j];
+                                            float (*tile)[kTP], int lane) {
     const int m = mbase + lane;
     if (t) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             const int n = nbase + j;
-            if (m < M && n < N && !(skip_lower && n < m)) p[(long long)n * ld + m] = x[j];
+            if (m < M && n < N && !(skip_lower && n < m)) p[(long long)n * ld + m] = lo_or(v[j], lo);
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tile[lane][j] = x[j];
+        for (int j4 = 0; j4 < 32; j4 += 4)
+            *reinterpret_cast<float4*>(&tile[lane][j4]) =
+                make_float4(lo_or(v[j4], lo), lo_or(v[j4 + 1], lo), lo_or(v[j4 + 2], lo), lo_or(v[j4 + 3], lo));
         __syncwarp();
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-            const int mm = mbase + i, n = nbase + lane;
-            if (mm < M && n < N && !(skip_lower && n < mm)) p[(long long)mm * ld + n] = tile[i][lane];
+        const int c = (lane & 7) * 4;
+        const bool vec = ((reinterpret_cast<uintptr_t>(p) | (uintptr_t)(ld * 4)) & 15) == 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int mm = mbase + i * 4 + (lane >> 3), n = nbase + c;
+            const float4 q = *reinterpret_cast<const float4*>(&tile[i * 4 + (lane >> 3)][c]);
+            if (vec && mm < M && n + 3 < N && !(skip_lower && n < mm)) {
+                *reinterpret_cast<float4*>(p + (long long)mm * ld + n) = q;
+            } else {
+                const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (mm < M && n + u < N && !(skip_lower && n + u < mm)) p[(long long)mm * ld + n + u] = e[u];
+            }
         }
         __syncwarp();
     }
@@ -198,20 +249,10 @@ __device__ __forceinline__ void chunk_store(const float (&v)[32], float* p, long
         for (int j = 0; j < 32; ++j) {
             const int n = nbase + j;
             if (m < M && n < N && n > m) {
-                if (t) p[(long long)m * ld + n] = x[j];
-                else p[(long long)n * ld + m] = x[j];
+                if (t) p[(long long)m * ld + n] = lo_or(v[j], lo);
+                else p[(long long)n * ld + m] = lo_or(v[j], lo);
             }
         }
-    }
-}
-
-__device__ __forceinline__ void store_outputs(const TcProb& pr, int m, int n, float v) {
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-        if (!pr.o[o]) continue;
-        const float x = pr.is_lo[o] ? v - tf32_trunc(v) : v;
-        if (pr.to[o]) pr.o[o][(long long)n * pr.ldo[o] + m] = x;
-        else pr.o[o][(long long)m * pr.ldo[o] + n] = x;
     }
 }
 
@@ -223,8 +264,8 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
     SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStages * kStageBytes);
-    float (*stage_tiles)[32][33] =
-        reinterpret_cast<float (*)[32][33]>(smem + kStages * kStageBytes + kBarrierBytes);
+    float (*stage_tiles)[32][36] =
+        reinterpret_cast<float (*)[32][36]>(smem + kStages * kStageBytes + kBarrierBytes);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int t_begin = cta_begin[blockIdx.x], t_end = cta_begin[blockIdx.x + 1];
 
@@ -316,13 +357,17 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             const TcProb& pr = probs[tl.prob];
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(&bars->tmem_full[acc], acc_phase);
-            tc_fence_after();
             const int mbase = tl.m0 + q * 32;
             const int m = mbase + lane;
             const bool diag = pr.sym && tl.m0 == tl.n0;
             const int nlim = min(pr.N, tl.n0 + pr.n_tile);
-            float (*tile)[33] = stage_tiles[warp - 2];
+            float (*tile)[kTP] = stage_tiles[warp - 2];
+            // prefetch the first Cin chunk (row-major axpy input, e.g. the EA factor) before the accumulator is ready
+            const bool pf = pr.beta != 0.f && pr.cin_t == 0 && pr.ksplit <= 1;
+            float4 pre[8];
+            if (pf) rm_issue(pre, pr.Cin, pr.ldcin, mbase, tl.n0, pr.M, nlim, lane);
+            mbar_wait(&bars->tmem_full[acc], acc_phase);
+            tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kMaxBN;
             for (int c0 = 0; c0 < pr.n_tile; c0 += 32) {
                 uint32_t r[32];
@@ -351,7 +396,12 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 }
                 if (pr.beta != 0.f) {
                     float cv[32];
-                    chunk_load(cv, pr.Cin, pr.ldcin, pr.cin_t, mbase, nbase, pr.M, nlim, tile, lane);
+                    if (pf) {
+                        rm_finish(cv, pre, tile, lane);
+                        if (c0 + 32 < pr.n_tile) rm_issue(pre, pr.Cin, pr.ldcin, mbase, nbase + 32, pr.M, nlim, lane);
+                    } else {
+                        chunk_load(cv, pr.Cin, pr.ldcin, pr.cin_t, mbase, nbase, pr.M, nlim, tile, lane);
+                    }
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = fmaf(pr.beta, cv[j], v[j]);
                 }
