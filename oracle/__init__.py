@@ -37,9 +37,10 @@ class OracleError(RuntimeError):
         self.code = code
 
 
-def build() -> None:
-    """Compile the checker (the C restatement, and oracle/_ref when /root/reference is present)."""
-    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+def build(targets=("all",)) -> None:
+    """Compile the checker (the C restatement, and oracle/_ref when /root/reference is present; "dropin" builds the
+    C++ drop-in check against the reference headers and the CUDA library)."""
+    subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
 _dp = C.POINTER(C.c_double)

@@ -1,0 +1,69 @@
+// dropin_test.cpp -- the C++ drop-in (include/rkfac_gpu.hpp) exercised against the UNMODIFIED reference headers:
+// the same inputs and RngState go through rkfac::X (reference, FP64 CPU) and rkfac::gpu::X (B200), and the
+// sign-invariant reconstruction, eigenvalues and preconditioned gradient are compared (test infrastructure;
+// built by oracle/Makefile into oracle/_ref/dropin_test, run by tests/test_gpu_dropin.py on the GPU box).
+#include <rkfac/kfactor.hpp>
+#include <rkfac/rnla.hpp>
+#include <rkfac/rng.hpp>
+
+#include <cmath>
+#include <cstdio>
+
+#include "rkfac_gpu.hpp"
+
+using namespace rkfac;
+
+static double rel(const DenseMatrix& a, const DenseMatrix& b) {
+    return frobenius_norm(subtract(a, b)) / std::max(1e-300, frobenius_norm(b));
+}
+
+int main() {
+    // config-1-like factor: zero-init EA of 12 steps of X^T X / n with column decay i^-1
+    const std::size_t d = 384, n = 192;
+    EAKFactor f_cpu(d, 0.95, /*zero_init=*/true), f_gpu(d, 0.95, true);
+    for (std::size_t k = 0; k < 12; ++k) {
+        RngState g = RngState(220615397).substream(k, 0);
+        DenseMatrix z = sample_gaussian(g, n, d);
+        DenseMatrix m(d, n);
+        for (std::size_t i = 0; i < d; ++i)
+            for (std::size_t s = 0; s < n; ++s) m(i, s) = z(s, i) / double(i + 1) / std::sqrt(double(n));
+        ea_update(f_cpu, m);
+        gpu::ea_update(f_gpu, m);
+    }
+    const double e_ea = rel(f_gpu.mbar, f_cpu.mbar);
+    int fails = e_ea < 1e-5 ? 0 : 1;
+    std::printf("{\"ea_rel\": %.3e", e_ea);
+
+    const SketchParams sk{48, 8, 2};
+    RngState g_j = RngState(99).substream(0, 0);
+    const DenseMatrix j = sample_gaussian(g_j, d, d);
+    for (int meth = 0; meth < 2; ++meth) {
+        RngState r0 = RngState(7).substream(0, 0), r1 = r0;
+        LowRankEig a = meth == 0 ? srevd(f_cpu.mbar, sk, r0) : rsvd_psd(f_cpu.mbar, sk, r0);
+        LowRankEig b = meth == 0 ? gpu::srevd(f_cpu.mbar, sk, r1) : gpu::rsvd_psd(f_cpu.mbar, sk, r1);
+        const double e_rec = rel(lowrank_reconstruct(b), lowrank_reconstruct(a));
+        double e_eig = 0.0;
+        for (std::size_t i = 0; i < a.d.size(); ++i) e_eig = std::max(e_eig, std::abs(a.d[i] - b.d[i]) / a.d[i]);
+        const DenseMatrix sa = apply_lowrank_damped_inverse(
+            a, 0.1, apply_lowrank_damped_inverse(a, 0.1, j, ApplySide::RIGHT), ApplySide::LEFT);
+        const DenseMatrix sb = gpu::apply_lowrank_damped_inverse(
+            b, 0.1, gpu::apply_lowrank_damped_inverse(b, 0.1, j, ApplySide::RIGHT), ApplySide::LEFT);
+        const double e_s = rel(sb, sa);
+        const bool ok = r0.counter == r1.counter && e_rec < 1e-4 && e_eig < 1e-4 && e_s < 1e-4 &&
+                        b.method == a.method && b.rank() == a.rank();
+        fails += ok ? 0 : 1;
+        std::printf(", \"%s\": {\"recon\": %.3e, \"eig\": %.3e, \"precond\": %.3e, \"counter_match\": %d}",
+                    meth == 0 ? "srevd" : "rsvd_psd", e_rec, e_eig, e_s, int(r0.counter == r1.counter));
+    }
+    // error behaviour mirrors the reference exceptions
+    bool threw = false;
+    try {
+        LowRankEig lr{DenseMatrix::identity(2), {1.0, 1.0}, DecompMethod::RSVD};
+        gpu::apply_lowrank_damped_inverse(lr, 0.0, DenseMatrix(2, 1, 1.0), ApplySide::LEFT);
+    } catch (const DampingNonpositive&) {
+        threw = true;
+    }
+    fails += threw ? 0 : 1;
+    std::printf(", \"damping_throws\": %d, \"fails\": %d}\n", int(threw), fails);
+    return fails == 0 ? 0 : 1;
+}

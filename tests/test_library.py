@@ -73,3 +73,14 @@ def test_rng_helpers_match_the_oracle(port):
     for s, a, b in ((7, 0, 0), (7, 0, 1), (220615397, 19, 31), (2**63 + 5, 2**40, 3)):
         assert rk.substream_seed(s, a, b) == port.substream(s, a, b)
     assert rk.splitmix64(0) == port.splitmix64(0)
+
+
+def test_cpp_dropin_compiles_against_reference_headers():
+    """include/rkfac_gpu.hpp compiles with the unmodified reference headers (the C++ drop-in boundary)."""
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers not present on this machine")
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")
+    out = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", ref_inc, "-I", os.path.join(ROOT, "include"),
+                          "-I", "/usr/local/cuda/include", src], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr[-2000:]
