@@ -400,7 +400,11 @@ __global__ void __launch_bounds__(256) backxform_kernel(const EigDesc* __restric
     }
     for (long long e = tid; e < (long long)n * kBxCols; e += blockDim.x) {
         const int i = (int)(e / kBxCols), c = (int)(e % kBxCols);
-        if (c < nc) ed.P[(long long)i * ed.ldp + c0 + c] = (float)Zs[e];
+        if (c < nc) {
+            const float v = (float)Zs[e];
+            ed.Pt[(long long)(c0 + c) * ed.ldpt + i] = v;
+            ed.Ptlo[(long long)(c0 + c) * ed.ldpt + i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        }
     }
 }
 

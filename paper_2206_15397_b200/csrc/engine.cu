@@ -12,6 +12,7 @@
 //   eig        FP64 tridiagonal workspace, P (w x r FP32) eigenvectors of the core
 //   Ut         r x d FP32 caller-owned U^T, dvals r FP32 (LowRankEig, rnla.hpp:17-24)
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 
@@ -58,7 +59,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
     Carver c;
     struct Offs {
         size_t S[2][4], Xc, Xl, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
-            scr, piv, z, P, scale, zflags, bracket;
+            scr, piv, z, Pt, Ptlo, scale, zflags, bracket, Uti, Utilo, Ui, Uilo;
     };
     std::vector<Offs> offs(n);
     for (int i = 0; i < n; ++i) {
@@ -105,10 +106,16 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         o.scr = c.take<double>(4 * w * rr);
         o.piv = c.take<unsigned char>(w * rr);
         o.z = c.take<double>(w * rr);
-        o.P = c.take<float>(w * rr);
+        o.Pt = c.take<float>(rr * wp);
+        o.Ptlo = c.take<float>(rr * wp);
         o.scale = c.take<float>(rr);
         o.zflags = c.take<int>(rr + 1);
         o.bracket = c.take<float>(rr);
+        F.rp = (F.r + 3) / 4 * 4;
+        o.Uti = c.take<float>(rr * dp);
+        o.Utilo = c.take<float>(rr * dp);
+        o.Ui = c.take<float>(d * F.rp);
+        o.Uilo = c.take<float>(d * F.rp);
     }
     arena_.alloc(c.off);
     RKFAC_CUDA(cudaMemset(arena_.p, 0, c.off));
@@ -133,8 +140,10 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         F.dvec = at<double>(arena_, o.dvec); F.evec = at<double>(arena_, o.evec);
         F.evals = at<double>(arena_, o.evals); F.scr = at<double>(arena_, o.scr);
         F.piv = at<unsigned char>(arena_, o.piv); F.z = at<double>(arena_, o.z);
-        F.P = at<float>(arena_, o.P); F.scale = at<float>(arena_, o.scale);
+        F.Pt = at<float>(arena_, o.Pt); F.Ptlo = at<float>(arena_, o.Ptlo); F.scale = at<float>(arena_, o.scale);
         F.zflags = at<int>(arena_, o.zflags); F.bracket = at<float>(arena_, o.bracket);
+        F.Uti = at<float>(arena_, o.Uti); F.Utilo = at<float>(arena_, o.Utilo);
+        F.Ui = at<float>(arena_, o.Ui); F.Uilo = at<float>(arena_, o.Uilo);
     }
 }
 
@@ -208,7 +217,7 @@ void Plan::bind_layers(int nl, const int* a, const int* g, const float* const* J
                        float* const* mid) {
     layers_.assign(nl, LayerState{});
     Carver c;
-    std::vector<size_t> o1(nl), o2(nl);
+    std::vector<std::array<size_t, 8>> o(nl);
     for (int l = 0; l < nl; ++l) {
         RKFAC_REQUIRE(a[l] >= 0 && a[l] < nfactors() && g[l] >= 0 && g[l] < nfactors(), RKFAC_INVALID_ARGUMENT,
                       "layer factor index out of range");
@@ -216,14 +225,32 @@ void Plan::bind_layers(int nl, const int* a, const int* g, const float* const* J
         L.a = a[l]; L.g = g[l];
         L.J = J[l]; L.out = out[l]; L.mid = mid[l];
         const FactorState &A = f_[L.a], &G = f_[L.g];
-        o1[l] = c.take<float>((size_t)G.d * A.r);
-        o2[l] = c.take<float>((size_t)G.r * A.d);
+        const size_t dAp = (A.d + 3) / 4 * 4, dGp = (G.d + 3) / 4 * 4;
+        o[l][0] = c.take<float>((size_t)G.d * dAp);
+        o[l][1] = c.take<float>((size_t)G.d * dAp);
+        o[l][2] = c.take<float>((size_t)G.d * A.rp);
+        o[l][3] = c.take<float>((size_t)G.d * A.rp);
+        o[l][4] = c.take<float>((size_t)A.d * dGp);
+        o[l][5] = c.take<float>((size_t)A.d * dGp);
+        o[l][6] = c.take<float>((size_t)A.d * G.rp);
+        o[l][7] = c.take<float>((size_t)A.d * G.rp);
     }
     layer_arena_.alloc(c.off);
+    std::vector<SplitDesc> sj;
+    long long off = 0;
     for (int l = 0; l < nl; ++l) {
-        layers_[l].W1 = at<float>(layer_arena_, o1[l]);
-        layers_[l].W2 = at<float>(layer_arena_, o2[l]);
+        LayerState& L = layers_[l];
+        L.Jc = at<float>(layer_arena_, o[l][0]); L.Jlo = at<float>(layer_arena_, o[l][1]);
+        L.W1 = at<float>(layer_arena_, o[l][2]); L.W1lo = at<float>(layer_arena_, o[l][3]);
+        L.Mt = at<float>(layer_arena_, o[l][4]); L.Mtlo = at<float>(layer_arena_, o[l][5]);
+        L.W2t = at<float>(layer_arena_, o[l][6]); L.W2tlo = at<float>(layer_arena_, o[l][7]);
+        const FactorState &A = f_[L.a], &G = f_[L.g];
+        const long long dAp = (A.d + 3) / 4 * 4;
+        sj.push_back(SplitDesc{L.J, L.Jc, L.Jlo, G.d, A.d, A.d, dAp, off});
+        off += (long long)G.d * A.d;
     }
+    upload(d_split_j_, sj);
+    split_j_total_ = off;
     ap_lambda_ = -1;
 }
 
@@ -261,7 +288,7 @@ void Plan::build_decomp_stages() {
         core_[dir] = std::make_unique<TcGemm>();
         gram64_[dir] = std::make_unique<GemmBatch>(GemmKind::F32_ACC64);
         tri64_[dir] = std::make_unique<GemmBatch>(GemmKind::F64_F32);
-        lift_[dir] = std::make_unique<GemmBatch>(GemmKind::F32);
+        lift_[dir] = std::make_unique<TcGemm>();
         std::vector<CompleteDesc> comp;
         std::vector<SplitDesc> st;
         long long st_off = 0;
@@ -316,11 +343,19 @@ void Plan::build_decomp_stages() {
                 cc.out0 = out_r(F.core, F.w);
                 core_[dir]->add(cc);
             }
-            // lift: srevd U^T = P_r^T Q^T (rnla.hpp:101); rsvd U^T = diag(1/s) P_r^T Y^T (eig.hpp:260-266)
-            const float* Bop = method_ == RKFAC_SREVD ? Q.T : Y.T;
-            GemmDesc ld = GemmBatch::make(F.r, F.d, F.w, F.P, F.r, 1, Bop, F.dp, 0, F.Ut, F.ldu, 0);
-            if (method_ == RKFAC_RSVD) ld.rs = F.scale;
-            lift_[dir]->add(ld);
+            // lift: srevd U = Q P_r (rnla.hpp:101); rsvd U = Y P_r diag(1/s) (eig.hpp:260-266); both layouts of U
+            // (+ lo planes) for the apply stage, U^T copied out to the caller afterwards
+            {
+                TcProblemDesc lf;
+                lf.M = F.d; lf.N = F.r; lf.K = F.w;
+                const Role& Aop = method_ == RKFAC_SREVD ? Q : Y;
+                lf.A = Aop.R; lf.A_lo = Aop.Rlo; lf.lda = F.wp;
+                lf.B = F.Pt; lf.B_lo = F.Ptlo; lf.ldb = F.wp;
+                if (method_ == RKFAC_RSVD) lf.cs = F.scale;
+                lf.out0 = out_t(F.Uti, F.dp); lf.lo0 = out_t(F.Utilo, F.dp);
+                lf.out1 = out_r(F.Ui, F.rp); lf.lo1 = out_r(F.Uilo, F.rp);
+                lift_[dir]->add(lf);
+            }
         }
         // complete_[dir] completes the output of orth(src = dir), i.e. role S[dir ^ 1]
         upload(d_complete_[dir], comp);
@@ -329,6 +364,14 @@ void Plan::build_decomp_stages() {
         xq_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
+    std::vector<CopyDesc> cp;
+    long long cp_off = 0;
+    for (auto& F : f_) {
+        cp.push_back(CopyDesc{F.Uti, F.Ut, F.r, F.d, F.dp, F.ldu, cp_off});
+        cp_off += (long long)F.r * F.d;
+    }
+    upload(d_copy_ut_, cp);
+    copy_ut_total_ = cp_off;
     std::vector<CholDesc> c64, c32;
     std::vector<EigDesc> eg;
     std::vector<PostDesc> po;
@@ -340,10 +383,10 @@ void Plan::build_decomp_stages() {
         EigDesc e{};
         e.n = F.w; e.r = F.r; e.A = F.core; e.lda = F.w; e.scratch = F.eig_scratch; e.refl = F.refl;
         e.tau = F.tau; e.dvec = F.dvec; e.evec = F.evec; e.evals = F.evals; e.scr = F.scr; e.piv = F.piv;
-        e.z = F.z; e.P = F.P; e.ldp = F.r;
+        e.z = F.z; e.Pt = F.Pt; e.Ptlo = F.Ptlo; e.ldpt = F.wp;
         eg.push_back(e);
         po.push_back(PostDesc{F.r, method_, F.evals, F.dvals, F.scale, F.zflags, F.zflags + F.r});
-        cu.push_back(CompleteDesc{F.r, F.d, F.ldu, F.Ut, F.zflags, F.zflags + F.r, nullptr, nullptr, nullptr, 0});
+        cu.push_back(CompleteDesc{F.r, F.d, F.dp, F.Uti, F.zflags, F.zflags + F.r, F.Utilo, F.Ui, F.Uilo, F.rp});
         br.push_back(BracketDesc{F.r, F.dvals, F.bracket});
     }
     upload(d_chol64_, c64);
@@ -399,25 +442,45 @@ void Plan::build_ea_stage(double rho, double scale) {
 }
 
 void Plan::build_apply_stages(double lambda) {
-    for (auto& a : ap_) a = std::make_unique<GemmBatch>(GemmKind::F32);
-    const double inv = 1.0 / lambda;
+    // Four grouped 3xTF32 tcgen05 GEMMs over all layers, every operand K-major (intermediates are written in the
+    // layout their consumer needs, with their TF32 lo planes):
+    //   RIGHT (kfactor.hpp:156-160):  W1 = J U_A diag(b_A)           (M=dG, N=rA, K=dA)
+    //                                 mid^T = (W1 U_A^T + J/lambda)^T (M=dG, N=dA, K=rA)
+    //   LEFT  (kfactor.hpp:147-152):  W2^T = (diag(b_G) U_G^T mid)^T  (M=rG, N=dA, K=dG)
+    //                                 out = U_G W2 + mid/lambda        (M=dG, N=dA, K=rG)
+    for (auto& a : ap_) a = std::make_unique<TcGemm>();
+    const float inv = (float)(1.0 / lambda);
     for (auto& L : layers_) {
         const FactorState &A = f_[L.a], &G = f_[L.g];
-        // RIGHT (kfactor.hpp:156-160): W1 = J U_A diag(bracket_A); mid = W1 U_A^T + J / lambda
-        GemmDesc d0 = GemmBatch::make(G.d, A.r, A.d, L.J, A.d, 0, A.Ut, A.ldu, 1, L.W1, A.r, 0);
-        d0.cs = A.bracket;
-        ap_[0]->add(d0);
-        GemmDesc d1 = GemmBatch::make(G.d, A.d, A.r, L.W1, A.r, 0, A.Ut, A.ldu, 0, L.mid, A.d, 0);
-        d1.D = L.J; d1.ldd = A.d; d1.gamma = inv;
-        ap_[1]->add(d1);
-        // LEFT (kfactor.hpp:147-152): W2 = diag(bracket_G) U_G^T mid; out = U_G W2 + mid / lambda
-        GemmDesc d2 = GemmBatch::make(G.r, A.d, G.d, G.Ut, G.ldu, 0, L.mid, A.d, 0, L.W2, A.d, 0);
-        d2.rs = G.bracket;
-        d2.ksplit = choose_ksplit(G.r, A.d, G.d, 128, 128);
-        ap_[2]->add(d2);
-        GemmDesc d3 = GemmBatch::make(G.d, A.d, G.r, G.Ut, G.ldu, 1, L.W2, A.d, 0, L.out, A.d, 0);
-        d3.D = L.mid; d3.ldd = A.d; d3.gamma = inv;
-        ap_[3]->add(d3);
+        const long long dAp = (A.d + 3) / 4 * 4, dGp = (G.d + 3) / 4 * 4;
+        TcProblemDesc p0;
+        p0.M = G.d; p0.N = A.r; p0.K = A.d;
+        p0.A = L.Jc; p0.A_lo = L.Jlo; p0.lda = dAp;
+        p0.B = A.Uti; p0.B_lo = A.Utilo; p0.ldb = A.dp;
+        p0.cs = A.bracket;
+        p0.out0 = out_r(L.W1, A.rp); p0.lo0 = out_r(L.W1lo, A.rp);
+        ap_[0]->add(p0);
+        TcProblemDesc p1;
+        p1.M = G.d; p1.N = A.d; p1.K = A.r;
+        p1.A = L.W1; p1.A_lo = L.W1lo; p1.lda = A.rp;
+        p1.B = A.Ui; p1.B_lo = A.Uilo; p1.ldb = A.rp;
+        p1.gamma = inv; p1.Din = L.Jc; p1.lddin = dAp; p1.din_t = 0;
+        p1.out0 = out_t(L.Mt, dGp); p1.lo0 = out_t(L.Mtlo, dGp);
+        ap_[1]->add(p1);
+        TcProblemDesc p2;
+        p2.M = G.r; p2.N = A.d; p2.K = G.d;
+        p2.A = G.Uti; p2.A_lo = G.Utilo; p2.lda = G.dp;
+        p2.B = L.Mt; p2.B_lo = L.Mtlo; p2.ldb = dGp;
+        p2.rs = G.bracket;
+        p2.out0 = out_t(L.W2t, G.rp); p2.lo0 = out_t(L.W2tlo, G.rp);
+        ap_[2]->add(p2);
+        TcProblemDesc p3;
+        p3.M = G.d; p3.N = A.d; p3.K = G.r;
+        p3.A = G.Ui; p3.A_lo = G.Uilo; p3.lda = G.rp;
+        p3.B = L.W2t; p3.B_lo = L.W2tlo; p3.ldb = G.rp;
+        p3.gamma = inv; p3.Din = L.Mt; p3.lddin = dGp; p3.din_t = 1;
+        p3.out0 = out_r(L.out, A.d);
+        ap_[3]->add(p3);
     }
     for (auto& a : ap_) a->finalize();
     ap_lambda_ = lambda;
@@ -526,6 +589,7 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     launch_post(d_post_.as<PostDesc>(), n, s);
     lift_[y]->launch(s);
     if (method_ == RKFAC_RSVD) launch_complete(d_complete_u_.as<CompleteDesc>(), n, s);
+    launch_copy(d_copy_ut_.as<CopyDesc>(), n, copy_ut_total_, s);
     mark(kEig, false);
     mark(kDecompose, false);
 }
@@ -538,6 +602,7 @@ void Plan::precondition(double lambda) {
     cudaStream_t s = ctx_->stream;
     mark(kApply, true);
     launch_bracket(d_bracket_.as<BracketDesc>(), nfactors(), lambda, s);
+    launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, s);  // J -> aligned copy + lo
     for (auto& a : ap_) a->launch(s);
     mark(kApply, false);
 }

@@ -56,18 +56,26 @@ struct FactorState {
     double *eig_scratch = nullptr, *refl = nullptr, *tau = nullptr, *dvec = nullptr, *evec = nullptr,
            *evals = nullptr, *scr = nullptr, *z = nullptr;
     unsigned char* piv = nullptr;
-    float* P = nullptr;                  // w x r
+    float *Pt = nullptr, *Ptlo = nullptr;  // r x w (pitch wp): eigenvectors of the core, transposed
     float* scale = nullptr;              // r
     int* zflags = nullptr;               // r + 1
     float* bracket = nullptr;            // r
+    int rp = 0;                          // r rounded up to 4
+    // the basis in both K-major layouts (+ TF32 lo planes) for the tensor-core apply stage
+    float *Uti = nullptr, *Utilo = nullptr;  // r x d, pitch dp
+    float *Ui = nullptr, *Uilo = nullptr;    // d x r, pitch rp
 };
 
 struct LayerState {
     int a = 0, g = 0;
-    const float* J = nullptr;  // dG x dA
+    const float* J = nullptr;  // dG x dA (caller pitch dA)
     float* out = nullptr;
     float* mid = nullptr;
-    float *W1 = nullptr, *W2 = nullptr;  // plan-owned: dG x rA, rG x dA
+    // plan-owned, TMA-aligned (pitches rounded up to 4 floats)
+    float *Jc = nullptr, *Jlo = nullptr;       // dG x dA, pitch dAp
+    float *W1 = nullptr, *W1lo = nullptr;      // dG x rA, pitch rAp
+    float *Mt = nullptr, *Mtlo = nullptr;      // mid^T: dA x dG, pitch dGp
+    float *W2t = nullptr, *W2tlo = nullptr;    // W2^T: dA x rG, pitch rGp
 };
 
 class Plan {
@@ -121,14 +129,14 @@ class Plan {
     bool ea_tc_ = false;     // EA runs on the tensor-core path (needs TMA-valid X and samples)
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
-    std::unique_ptr<TcGemm> xq_[2], gram_[2], tri_[2], core_[2];
-    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2], lift_[2];
+    std::unique_ptr<TcGemm> xq_[2], gram_[2], tri_[2], core_[2], lift_[2];
+    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2];
     std::unique_ptr<TcGemm> ea_tc_stage_;
     std::unique_ptr<GemmBatch> ea_simt_;
-    std::unique_ptr<GemmBatch> ap_[4];
+    std::unique_ptr<TcGemm> ap_[4];
     DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
-    DevBuf d_split_x_, d_split_m_, d_split_t_[2], d_split_omega_;
-    long long split_x_total_ = 0, split_m_total_ = 0, split_t_total_ = 0;
+    DevBuf d_split_x_, d_split_m_, d_split_t_[2], d_split_omega_, d_split_j_, d_copy_ut_;
+    long long split_x_total_ = 0, split_m_total_ = 0, split_t_total_ = 0, split_j_total_ = 0, copy_ut_total_ = 0;
     std::vector<OmegaDesc> omega_;
     long long omega_total_ = 0;
     int wmax_ = 0, rmax_ = 0;

@@ -62,8 +62,9 @@ struct EigDesc {
     double* scr;         // 4*n*r inverse-iteration LU
     unsigned char* piv;  // n*r
     double* z;           // n x r tridiagonal eigenvectors
-    float* P;            // n x r eigenvectors of the core (FP32), ld = ldp
-    long long ldp;
+    float* Pt;           // r x n eigenvectors of the core, transposed (row c = eigenvector c), pitch ldpt
+    float* Ptlo;         // TF32 lo plane of Pt
+    long long ldpt;
 };
 size_t tridiag_smem_bytes(int nmax);
 void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaStream_t s);
@@ -90,6 +91,16 @@ struct BracketDesc {
     float* out;
 };
 void launch_bracket(const BracketDesc* d_descs, int n, double lambda, cudaStream_t s);
+
+// Grouped 2-D copy (all problems in one launch): dst[r*ldd + c] = src[r*lds + c], offset = prefix of rows*cols.
+struct CopyDesc {
+    const float* src;
+    float* dst;
+    int rows, cols;
+    long long lds, ldd;
+    long long offset;
+};
+void launch_copy(const CopyDesc* d_descs, int n, long long total, cudaStream_t s);
 
 // Transposed copy: out[j*ldo + i] = in[i*ldi + j] for an rows x cols input (used by the single-factor API to
 // return U in the reference's d x r layout).

@@ -76,6 +76,21 @@ __global__ void bracket_kernel(const BracketDesc* __restrict__ descs, double lam
     }
 }
 
+__global__ void copy_kernel(const CopyDesc* __restrict__ descs, int n, long long total) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (descs[mid].offset <= e) lo = mid; else hi = mid - 1;
+        }
+        const CopyDesc& cd = descs[lo];
+        const long long local = e - cd.offset;
+        const int r = (int)(local / cd.cols), c = (int)(local - (long long)r * cd.cols);
+        cd.dst[(long long)r * cd.ldd + c] = cd.src[(long long)r * cd.lds + c];
+    }
+}
+
 __global__ void transpose_kernel(const float* __restrict__ in, long long ldi, int rows, int cols,
                                  float* __restrict__ out, long long ldo) {
     __shared__ float tile[32][33];
@@ -112,6 +127,14 @@ void launch_post(const PostDesc* d_descs, int nfactors, cudaStream_t s) {
 void launch_bracket(const BracketDesc* d_descs, int n, double lambda, cudaStream_t s) {
     if (n == 0) return;
     bracket_kernel<<<n, 256, 0, s>>>(d_descs, lambda);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+}
+
+void launch_copy(const CopyDesc* d_descs, int n, long long total, cudaStream_t s) {
+    if (total == 0) return;
+    const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
+    copy_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }
