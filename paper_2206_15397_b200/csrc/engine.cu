@@ -286,12 +286,10 @@ void Plan::build_decomp_stages() {
         gram_[dir] = std::make_unique<TcGemm>();
         tri_[dir] = std::make_unique<TcGemm>();
         core_[dir] = std::make_unique<TcGemm>();
-        gram64_[dir] = std::make_unique<GemmBatch>(GemmKind::F32_ACC64);
-        tri64_[dir] = std::make_unique<GemmBatch>(GemmKind::F64_F32);
+        gram64_[dir] = std::make_unique<Gram64Batch>();
+        tri64_[dir] = std::make_unique<Tri64Batch>();
         lift_[dir] = std::make_unique<TcGemm>();
         std::vector<CompleteDesc> comp;
-        std::vector<SplitDesc> st;
-        long long st_off = 0;
         for (auto& F : f_) {
             Role& Y = F.S[dir];      // written by xq_[dir]; source of the orthonormalisation indexed dir
             Role& Q = F.S[dir ^ 1];  // basis read by xq_[dir]; destination of orth(src = dir)
@@ -322,16 +320,9 @@ void Plan::build_decomp_stages() {
                 t.out1 = out_r(Q.R, F.wp); t.lo1 = out_r(Q.Rlo, F.wp);
                 tri_[dir]->add(t);
             }
-            // FP64 CholeskyQR of Y into Q (SIMT): G = Y^T Y in FP64, Q^T = Linv Y^T with FP64 accumulation
-            {
-                GemmDesc g64 = GemmBatch::make(F.w, F.w, F.d, Y.T, F.dp, 0, Y.T, F.dp, 1, F.G64, F.w, 0);
-                // FP64 SIMT Gram: long K (= d) over only ceil(w/64)^2 tiles -> split K (fixed per shape: deterministic)
-                g64.ksplit = std::max(1, std::min(16, (int)ceil_div(F.d, 16) / 24));
-                gram64_[dir]->add(g64);
-                tri64_[dir]->add(GemmBatch::make(F.w, F.d, F.w, F.Linv64, F.wp, 0, Y.T, F.dp, 0, Q.T, F.dp, 0));
-                st.push_back(SplitDesc{Q.T, nullptr, Q.Tlo, F.w, F.d, F.dp, F.dp, st_off});
-                st_off += (long long)F.w * F.d;
-            }
+            // FP64 CholeskyQR of Y into Q (DMMA): G = Y^T Y in FP64, Q^T = Linv Y^T with FP64 accumulation
+            gram64_[dir]->add(F.w, F.d, Y.T, F.dp, F.G64, F.w);
+            tri64_[dir]->add(F.w, F.d, F.Linv64, F.wp, Y.T, F.dp, Q.T, Q.Tlo, F.dp);
             comp.push_back(CompleteDesc{F.w, F.d, F.dp, Q.T, F.flags, F.flags + F.w, Q.Tlo, Q.R, Q.Rlo, F.wp});
             // core: srevd C = Q^T (X Q) (rnla.hpp:97); rsvd_psd B B^T = Y^T Y (eig.hpp:251)
             {
@@ -359,8 +350,6 @@ void Plan::build_decomp_stages() {
         }
         // complete_[dir] completes the output of orth(src = dir), i.e. role S[dir ^ 1]
         upload(d_complete_[dir], comp);
-        upload(d_split_t_[dir], st);
-        split_t_total_ = st_off;
         xq_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
@@ -493,7 +482,6 @@ void Plan::orth(int src, bool fp64, cudaStream_t s) {
         gram64_[src]->launch(s);
         launch_cholinv(d_chol64_.as<CholDesc>(), n, wmax_, true, true, kTol64, s);
         tri64_[src]->launch(s);
-        launch_split(d_split_t_[src].as<SplitDesc>(), n, split_t_total_, s);
     } else {
         gram_[src]->launch(s);
         launch_cholinv(d_chol32_.as<CholDesc>(), n, wmax_, false, false, kTol32, s);

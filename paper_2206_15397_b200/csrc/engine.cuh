@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "dmma.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "tc_gemm.cuh"
@@ -130,13 +131,14 @@ class Plan {
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
     std::unique_ptr<TcGemm> xq_[2], gram_[2], tri_[2], core_[2], lift_[2];
-    std::unique_ptr<GemmBatch> gram64_[2], tri64_[2];
+    std::unique_ptr<Gram64Batch> gram64_[2];
+    std::unique_ptr<Tri64Batch> tri64_[2];
     std::unique_ptr<TcGemm> ea_tc_stage_;
     std::unique_ptr<GemmBatch> ea_simt_;
     std::unique_ptr<TcGemm> ap_[4];
     DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
-    DevBuf d_split_x_, d_split_m_, d_split_t_[2], d_split_omega_, d_split_j_, d_copy_ut_;
-    long long split_x_total_ = 0, split_m_total_ = 0, split_t_total_ = 0, split_j_total_ = 0, copy_ut_total_ = 0;
+    DevBuf d_split_x_, d_split_m_, d_split_omega_, d_split_j_, d_copy_ut_;
+    long long split_x_total_ = 0, split_m_total_ = 0, split_j_total_ = 0, copy_ut_total_ = 0;
     std::vector<OmegaDesc> omega_;
     long long omega_total_ = 0;
     int wmax_ = 0, rmax_ = 0;
