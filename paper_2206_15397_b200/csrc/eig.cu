@@ -7,10 +7,12 @@
 //   tridiag_kernel   -- Householder tridiagonalisation, one CTA per factor, packed lower triangle in shared
 //                       memory (FP64 keeps the normwise backward error ~1e-16*||C||, i.e. ~1e-12 relative on the
 //                       smallest retained eigenvalue of config 2).
-//   tdeig_kernel     -- one thread per wanted eigenpair: bisection with Sturm counts (the k-th largest
-//                       eigenvalue, so the output is already sorted descending like sort_desc_stable,
-//                       eig.hpp:197-203), then inverse iteration with partial-pivoting LU; clusters of (near)
-//                       equal eigenvalues are re-orthogonalised (modified Gram-Schmidt).
+//   bisect_kernel    -- 4 threads per wanted eigenvalue (5-section per step), grid (eigenvalue chunk, factor):
+//                       division-free Sturm counts for the k-th largest eigenvalue, so the output is already
+//                       sorted descending like sort_desc_stable (eig.hpp:197-203).
+//   eigvec_kernel    -- one thread per eigenpair: twisted factorisation (one solve) for isolated eigenvalues,
+//                       inverse iteration (partial-pivoting LU) for members of clusters.
+//   reorth_kernel    -- modified Gram-Schmidt over clusters of (near) equal eigenvalues.
 //   backxform_kernel -- P = H_0 ... H_{n-3} Z, the eigenvectors of the core.
 // The cost is O(w^3) FP64 once (tridiagonalisation) instead of O(sweeps * w^3) for Jacobi; see DESIGN.md.
 #include <cfloat>
@@ -145,198 +147,384 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(const EigDesc* __restrict
 }
 
 // ------------------------------------------------------------------------------------- tridiagonal eig
-// Number of eigenvalues of T strictly less than x (Sturm count, LAPACK dstebz style with pivmin guard).
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
-    int cnt = 0;
-    double q = d[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    if (q < 0.0) ++cnt;
-    for (int i = 1; i < n; ++i) {
-        q = d[i] - x - e2[i - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        if (q < 0.0) ++cnt;
+// Spread over the whole GPU: grid (eigenvalue chunk, factor) for both the bisection and the vectors.
+
+// Sturm count (eigenvalues of T strictly below x) with the division-free three-term recurrence of the leading
+// principal minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}; the count is the number of sign changes, i.e. of
+// negative pivots q_i = p_i / p_{i-1} of the LDL^T recurrence LAPACK dstebz uses.  d, e2 are pre-scaled to
+// ||T|| ~ 1 and negligible e are zero (dstebz's relative splitting test).  The fast loop has a single FMA on its
+// dependence chain: e^2 p_{i-2} is formed a step ahead, the sign bookkeeping runs on the integer pipe, and every 4
+// steps both minors are renormalised by the power of two that brings p_{i-1} (known a step early) to [1, 2).
+// An exactly zero minor (x on an eigenvalue of a leading block) is only flagged in the fast loop; the rare flagged
+// count is redone with dstebz's guard (a zero pivot becomes -pivmin: here p_i = -2^-200 p_{i-1}).
+__device__ __forceinline__ double pow2_inverse_of(double v) {  // 2^-floor(log2|v|), clamped to the normal range
+    const int eb = (__double2hiint(v) >> 20) & 0x7ff;
+    return __hiloint2double((2046 - max(1, min(eb, 2045))) << 20, 0);
+}
+
+template <bool kGuard>
+__device__ __forceinline__ void sturm_step(double dx, double e2, double& p0, double& p1, int& cnt, int& zero) {
+    double pn = fma(dx, p1, -e2 * p0);
+    if (kGuard) {
+        if (pn == 0.0) pn = -0x1p-200 * p1;
+    } else {
+        zero |= (__double2hiint(pn) << 1) == 0;  // +-0 (or a denormal: harmless, just takes the guarded path)
     }
+    cnt += (int)((unsigned)(__double2hiint(pn) ^ __double2hiint(p1)) >> 31);
+    p0 = p1;
+    p1 = pn;
+}
+
+template <bool kGuard>
+__device__ __forceinline__ int sturm_count_impl(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                                double x, int& zero) {
+    double p0 = 1.0, p1 = d[0] - x;
+    if (p1 == 0.0) p1 = -0x1p-200;
+    int cnt = p1 < 0.0;
+    int i = 1;
+    for (; i + 3 < n; i += 4) {
+        const double d0 = d[i], d1 = d[i + 1], d2 = d[i + 2], d3 = d[i + 3];
+        const double f0 = e2[i - 1], f1 = e2[i], f2 = e2[i + 1], f3 = e2[i + 2];
+        sturm_step<kGuard>(d0 - x, f0, p0, p1, cnt, zero);
+        sturm_step<kGuard>(d1 - x, f1, p0, p1, cnt, zero);
+        sturm_step<kGuard>(d2 - x, f2, p0, p1, cnt, zero);
+        const double f = pow2_inverse_of(p1);  // p1 here is p0 after the next step
+        sturm_step<kGuard>(d3 - x, f3, p0, p1, cnt, zero);
+        p0 *= f;
+        p1 *= f;
+    }
+    for (; i < n; ++i) sturm_step<kGuard>(d[i] - x, e2[i - 1], p0, p1, cnt, zero);
     return cnt;
 }
 
-__global__ void __launch_bounds__(256) tdeig_kernel(const EigDesc* __restrict__ descs) {
-    const EigDesc& ed = descs[blockIdx.x];
+__device__ __forceinline__ int sturm_count_p(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                             double x) {
+    int zero = 0;
+    const int c = sturm_count_impl<false>(d, e2, n, x, zero);
+    if (!zero) return c;
+    return sturm_count_impl<true>(d, e2, n, x, zero);
+}
+
+constexpr int kBisG = 4;    // threads per eigenvalue: 5-section per iteration
+constexpr int kBisE = 32;   // eigenvalues per CTA
+constexpr int kBisThreads = kBisG * kBisE;
+
+// Gershgorin interval and norm of T, computed by the first W lanes of warp 0 (n <= 512).
+template <int W = 32>
+__device__ void tri_bounds(const double* d, const double* e, int n, double* out /* lo, hi, tnorm */) {
+    constexpr unsigned mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+    const int lane = threadIdx.x & 31;
+    double lo = DBL_MAX, hi = -DBL_MAX, tn = 0.0;
+    for (int i = lane; i < n; i += W) {
+        const double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
+        lo = fmin(lo, d[i] - off);
+        hi = fmax(hi, d[i] + off);
+        tn = fmax(tn, fabs(d[i]) + off);
+    }
+    for (int o = W / 2; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(mask, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(mask, hi, o));
+        tn = fmax(tn, __shfl_xor_sync(mask, tn, o));
+    }
+    if (lane == 0) { out[0] = lo; out[1] = hi; out[2] = fmax(tn, DBL_MIN); }
+}
+
+__global__ void __launch_bounds__(kBisThreads) bisect_kernel(const EigDesc* __restrict__ descs) {
+    const EigDesc& ed = descs[blockIdx.y];
     const int n = ed.n, r = ed.r;
-    __shared__ double d[kMaxN], e[kMaxN], e2[kMaxN], lam[kMaxN];
-    __shared__ double s_lo, s_hi, s_pivmin, s_tnorm;
+    const int kbase = blockIdx.x * kBisE;
+    if (kbase >= r) return;
+    __shared__ double d[kMaxN], e2[kMaxN], ev[kMaxN], bnd[3];
     const int tid = threadIdx.x;
     for (int i = tid; i < n; i += blockDim.x) {
         d[i] = ed.dvec[i];
-        e[i] = (i < n - 1) ? ed.evec[i] : 0.0;
-        e2[i] = e[i] * e[i];
+        ev[i] = (i < n - 1) ? ed.evec[i] : 0.0;
     }
     __syncthreads();
-    if (tid == 0) {
-        double lo = DBL_MAX, hi = -DBL_MAX, emax2 = 0.0, tn = 0.0;
-        for (int i = 0; i < n; ++i) {
-            const double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
-            lo = fmin(lo, d[i] - off);
-            hi = fmax(hi, d[i] + off);
-            emax2 = fmax(emax2, e2[i]);
-            tn = fmax(tn, fabs(d[i]) + off);
+    if (tid < 32) tri_bounds(d, ev, n, bnd);
+    __syncthreads();
+    int ex;
+    frexp(bnd[2], &ex);
+    const double sc = ldexp(1.0, -ex);  // exact: ||T|| sc in [0.5, 1)
+    const double lo0 = bnd[0], hi0 = bnd[1], tnorm = bnd[2];
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+        const double di = d[i] * sc;
+        double t = 0.0;
+        if (i < n - 1) {
+            const double ei = ev[i] * sc, dn = ed.dvec[i + 1] * sc;
+            t = ei * ei;
+            if (t <= DBL_EPSILON * DBL_EPSILON * fabs(di * dn) + DBL_MIN) t = 0.0;  // dstebz split test
         }
-        const double pivmin = DBL_MIN * fmax(1.0, emax2);
-        const double pad = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin;
-        s_lo = lo - pad;
-        s_hi = hi + pad;
-        s_pivmin = pivmin;
-        s_tnorm = fmax(tn, DBL_MIN);
+        d[i] = di;
+        e2[i] = t;
     }
     __syncthreads();
-    const double pivmin = s_pivmin, tnorm = s_tnorm;
 
-    // Multisection for the k-th largest eigenvalue (ascending index n-1-k): 4 Sturm counts per iteration run as
-    // independent chains (their divisions overlap), shrinking the bracket 5x per iteration instead of 2x.
-    for (int k = tid; k < r; k += blockDim.x) {
-        const int idx = n - 1 - k;
-        double lo = s_lo, hi = s_hi;
-        const double abstol = 4.0 * DBL_EPSILON * tnorm;
-        for (int it = 0; it < 100; ++it) {
-            if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + abstol) break;
-            const double h = (hi - lo) * 0.2;
-            double x[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = lo + h * (u + 1);
-            if (x[0] <= lo || x[3] >= hi) {  // bracket at the resolution of doubles: plain bisection step
-                const double mid = 0.5 * (lo + hi);
-                if (mid == lo || mid == hi) break;
-                if (sturm_count(d, e2, n, mid, pivmin) <= idx) lo = mid; else hi = mid;
-                continue;
-            }
-            double q[4];
-            int cnt[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                q[u] = d[0] - x[u];
-                if (fabs(q[u]) < pivmin) q[u] = -pivmin;
-                cnt[u] += q[u] < 0.0;
-            }
-            for (int i = 1; i < n; ++i) {
-                const double di = d[i], ei = e2[i - 1];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    q[u] = di - x[u] - ei / q[u];
-                    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
-                    cnt[u] += q[u] < 0.0;
-                }
-            }
-            // counts are nondecreasing in x: the eigenvalue lies in the first sub-interval whose right end has
-            // more than idx eigenvalues below it
-            double nlo = lo, nhi = hi;
-#pragma unroll
-            for (int u = 3; u >= 0; --u)
-                if (cnt[u] <= idx) { nlo = x[u]; break; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (cnt[u] > idx) { nhi = x[u]; break; }
-            lo = nlo;
-            hi = nhi;
+    const int grp = tid / kBisG, u = tid % kBisG;
+    const int k = kbase + grp;  // k-th largest eigenvalue
+    if (k >= r) return;         // whole groups leave together
+    const unsigned gmask = ((1u << kBisG) - 1u) << ((tid & 31) & ~(kBisG - 1));
+    const int idx = n - 1 - k;
+    const double pad = 2.0 * DBL_EPSILON * fmax(fabs(lo0), fabs(hi0)) * sc + 4.0 * DBL_MIN;
+    double lo = lo0 * sc - pad, hi = hi0 * sc + pad;
+    const double abstol = 4.0 * DBL_EPSILON * tnorm * sc;
+    for (int it = 0; it < 100; ++it) {
+        if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + abstol) break;
+        const double h = (hi - lo) * (1.0 / (kBisG + 1));
+        const double x0 = lo + h, xl = lo + h * kBisG;
+        if (!(x0 > lo) || !(xl < hi)) {  // at the resolution of doubles: one plain bisection step
+            const double mid = 0.5 * (lo + hi);
+            if (mid == lo || mid == hi) break;
+            const bool above = sturm_count_p(d, e2, n, mid) > idx;  // same on every lane of the group
+            if (above) hi = mid; else lo = mid;
+            continue;
         }
-        lam[k] = 0.5 * (lo + hi);
+        const double x = lo + h * (u + 1);
+        const bool above = sturm_count_p(d, e2, n, x) > idx;
+        const unsigned b = __ballot_sync(gmask, above) & gmask;
+        const int first = b ? (__ffs(b) - 1) - ((tid & 31) & ~(kBisG - 1)) : kBisG;  // first point above
+        const double nhi = first < kBisG ? lo + h * (first + 1) : hi;
+        const double nlo = first > 0 ? lo + h * first : lo;
+        lo = nlo;
+        hi = nhi;
     }
-    __syncthreads();
-    for (int k = tid; k < r; k += blockDim.x) ed.evals[k] = lam[k];
+    if (u == 0) ed.evals[k] = 0.5 * (lo + hi) / sc;
+}
 
-    // Inverse iteration: (T - lam I) z = b, LU with partial pivoting.  Scratch layout [i][k] (coalesced).
-    const long long S = r;
-    double* U1 = ed.scr;             // diagonal of U
-    double* U2 = ed.scr + n * S;     // first superdiagonal
-    double* U3 = ed.scr + 2 * n * S; // second superdiagonal
-    double* ML = ed.scr + 3 * n * S; // multipliers (sign bit unused), pivot flag in PV
-    double* Z = ed.z;                // n x r (row-major, column k = eigenvector k)
-    unsigned char* PV = ed.piv;      // n x r
-    for (int k = tid; k < r; k += blockDim.x) {
-        const double lmb = lam[k];
-        const double eps_piv = DBL_EPSILON * tnorm;
-        // Factor.
-        double a = d[0] - lmb;
-        double b = (n > 1) ? e[0] : 0.0;
+// Inverse iteration from a pseudo-random start (LU with partial pivoting, 3 solves): used for members of
+// clusters of (numerically) equal eigenvalues, whose vectors must span the cluster before the MGS pass.
+__device__ void inverse_iteration(const double* d, const double* e, int n, double lmb, double tnorm, int k,
+                                  const EigDesc& ed) {
+    const long long S = ed.r;
+    double* U1 = ed.scr;
+    double* U2 = ed.scr + n * S;
+    double* U3 = ed.scr + 2 * n * S;
+    double* ML = ed.scr + 3 * n * S;
+    double* Z = ed.z;
+    unsigned char* PV = ed.piv;
+    const double eps_piv = DBL_EPSILON * tnorm;
+    double a = d[0] - lmb;
+    double b = (n > 1) ? e[0] : 0.0;
+    for (int i = 0; i < n - 1; ++i) {
+        const double c = e[i];
+        const double anext = d[i + 1] - lmb;
+        const double bnext = (i + 1 < n - 1) ? e[i + 1] : 0.0;
+        if (fabs(a) >= fabs(c)) {
+            double piv = a;
+            if (piv == 0.0) piv = eps_piv;
+            const double mult = c / piv;
+            U1[i * S + k] = piv; U2[i * S + k] = b; U3[i * S + k] = 0.0;
+            ML[i * S + k] = mult; PV[i * S + k] = 0;
+            a = anext - mult * b;
+            b = bnext;
+        } else {
+            const double mult = a / c;
+            U1[i * S + k] = c; U2[i * S + k] = anext; U3[i * S + k] = bnext;
+            ML[i * S + k] = mult; PV[i * S + k] = 1;
+            a = b - mult * anext;
+            b = -mult * bnext;
+        }
+    }
+    U1[(n - 1) * S + k] = (a == 0.0) ? eps_piv : a;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t h = splitmix64(0x5EEDULL ^ ((uint64_t)k << 32) ^ (uint64_t)i);
+        Z[i * S + k] = (double)(h >> 11) * 0x1.0p-53 - 0.5;
+    }
+    for (int iter = 0; iter < 3; ++iter) {
         for (int i = 0; i < n - 1; ++i) {
-            const double c = e[i];              // sub-diagonal entry T[i+1][i]
-            const double anext = d[i + 1] - lmb; // diagonal of row i+1
-            const double bnext = (i + 1 < n - 1) ? e[i + 1] : 0.0;
-            if (fabs(a) >= fabs(c)) {
-                double piv = a;
-                if (piv == 0.0) piv = eps_piv;
-                const double mult = c / piv;
-                U1[i * S + k] = piv; U2[i * S + k] = b; U3[i * S + k] = 0.0;
-                ML[i * S + k] = mult; PV[i * S + k] = 0;
-                a = anext - mult * b;
-                b = bnext;
-            } else {
-                const double mult = a / c;
-                U1[i * S + k] = c; U2[i * S + k] = anext; U3[i * S + k] = bnext;
-                ML[i * S + k] = mult; PV[i * S + k] = 1;
-                a = b - mult * anext;
-                b = -mult * bnext;
-            }
+            const double zi = Z[i * S + k], zi1 = Z[(i + 1) * S + k];
+            const double mult = ML[i * S + k];
+            if (PV[i * S + k]) { Z[i * S + k] = zi1; Z[(i + 1) * S + k] = zi - mult * zi1; }
+            else { Z[(i + 1) * S + k] = zi1 - mult * zi; }
         }
-        U1[(n - 1) * S + k] = (a == 0.0) ? eps_piv : a;
-        // Start vector: deterministic pseudo-random, then 3 solves.
-        for (int i = 0; i < n; ++i) {
-            const uint64_t h = splitmix64(0x5EEDULL ^ ((uint64_t)k << 32) ^ (uint64_t)i);
-            Z[i * S + k] = (double)(h >> 11) * 0x1.0p-53 - 0.5;
+        double z2 = 0.0, z1 = 0.0, nrm = 0.0;
+        for (int i = n - 1; i >= 0; --i) {
+            double s = Z[i * S + k];
+            if (i + 1 < n) s -= U2[i * S + k] * z1;
+            if (i + 2 < n) s -= U3[i * S + k] * z2;
+            const double zi = s / U1[i * S + k];
+            Z[i * S + k] = zi;
+            z2 = z1; z1 = zi;
+            nrm = fmax(nrm, fabs(zi));
         }
-        for (int iter = 0; iter < 3; ++iter) {
-            // forward: apply L^{-1} P
-            for (int i = 0; i < n - 1; ++i) {
-                const double zi = Z[i * S + k], zi1 = Z[(i + 1) * S + k];
-                const double mult = ML[i * S + k];
-                if (PV[i * S + k]) { Z[i * S + k] = zi1; Z[(i + 1) * S + k] = zi - mult * zi1; }
-                else { Z[(i + 1) * S + k] = zi1 - mult * zi; }
-            }
-            // back substitution with U (diag, super1, super2)
-            double z2 = 0.0, z1 = 0.0;  // z[i+2], z[i+1]
-            double nrm = 0.0;
-            for (int i = n - 1; i >= 0; --i) {
-                double s = Z[i * S + k];
-                if (i + 1 < n) s -= U2[i * S + k] * z1;
-                if (i + 2 < n) s -= U3[i * S + k] * z2;
-                const double zi = s / U1[i * S + k];
-                Z[i * S + k] = zi;
-                z2 = z1; z1 = zi;
-                nrm = fmax(nrm, fabs(zi));
-            }
-            // rescale (avoid overflow) and normalise to unit 2-norm at the end
-            const double inv = (nrm > 0.0) ? 1.0 / nrm : 1.0;
-            double s2 = 0.0;
-            for (int i = 0; i < n; ++i) { const double z = Z[i * S + k] * inv; Z[i * S + k] = z; s2 += z * z; }
-            const double inv2 = 1.0 / sqrt(s2);
-            for (int i = 0; i < n; ++i) Z[i * S + k] *= inv2;
+        const double inv = (nrm > 0.0) ? 1.0 / nrm : 1.0;
+        double s2 = 0.0;
+        for (int i = 0; i < n; ++i) { const double z = Z[i * S + k] * inv; Z[i * S + k] = z; s2 += z * z; }
+        const double inv2 = 1.0 / sqrt(s2);
+        for (int i = 0; i < n; ++i) Z[i * S + k] *= inv2;
+    }
+}
+
+// 1/x from the MUFU approximation and two Newton steps (full double precision; x is a normal number here).
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double t = fma(-x, r, 1.0);
+    r = fma(r, t, r);
+    t = fma(-x, r, 1.0);
+    return fma(r, t, r);
+}
+
+// Eigenvectors of isolated eigenvalues from the twisted factorisation T - lam I = N_t Delta_t N_t^T (the stationary
+// L+ D+ L+^T and progressive U- D- U-^T recurrences, twist t = argmin |gamma_t|, gamma_t = D+_t + D-_t - (d_t - lam)),
+// then z_t = 1, z_i = -L+_i z_{i+1} (i < t), z_{i+1} = -U-_i z_i (i >= t): one solve, no start vector.  Cluster
+// members (gap <= 1e-10 ||T||, the MGS threshold below) take the inverse-iteration path instead.
+// One thread per eigenpair, 16 per CTA; the recurrences live in shared memory ([i][thread], conflict-free):
+// L+ (later overwritten by z_i, i < t) and D+ (overwritten by U- in the backward sweep, then by z_{i+1}, i >= t).
+constexpr int kVecThreads = 16;
+size_t eigvec_smem_bytes(int nmax) { return (size_t)2 * nmax * kVecThreads * sizeof(double); }
+
+__global__ void __launch_bounds__(kVecThreads) eigvec_kernel(const EigDesc* __restrict__ descs) {
+    const EigDesc& ed = descs[blockIdx.y];
+    const int n = ed.n, r = ed.r;
+    const int tid = threadIdx.x;
+    const int k = blockIdx.x * kVecThreads + tid;
+    __shared__ double d[kMaxN], e[kMaxN], bnd[3];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* Ls = reinterpret_cast<double*>(smem_raw);  // [n][kVecThreads]
+    double* Ws = Ls + (size_t)n * kVecThreads;
+    if (blockIdx.x * kVecThreads >= r) return;
+    for (int i = tid; i < n; i += kVecThreads) {
+        d[i] = ed.dvec[i];
+        e[i] = (i < n - 1) ? ed.evec[i] : 0.0;
+    }
+    __syncwarp(0xffffu);
+    tri_bounds<kVecThreads>(d, e, n, bnd);
+    __syncwarp(0xffffu);
+    const double tnorm = bnd[2];
+    if (k >= r) return;
+    const double lmb = ed.evals[k];
+    const double clus = 1e-10 * tnorm;
+    const bool clustered = (k > 0 && fabs(ed.evals[k - 1] - lmb) <= clus) ||
+                           (k + 1 < r && fabs(ed.evals[k + 1] - lmb) <= clus);
+    if (clustered) {
+        inverse_iteration(d, e, n, lmb, tnorm, k, ed);
+        return;
+    }
+    const double eps_piv = DBL_EPSILON * tnorm;
+#define L_(i) Ls[(i) * kVecThreads + tid]
+#define W_(i) Ws[(i) * kVecThreads + tid]
+    // stationary: D+_{i+1} = (d_{i+1} - lam) - e_i^2 / D+_i
+    double dp = d[0] - lmb;
+    if (fabs(dp) < DBL_MIN) dp = eps_piv;
+    int i = 0;
+    for (; i + 4 < n; i += 4) {
+        double ee[4], dd[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { ee[u] = e[i + u]; dd[u] = d[i + 1 + u] - lmb; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            W_(i + u) = dp;
+            const double l = ee[u] * rcp_nr(dp);
+            L_(i + u) = l;
+            dp = dd[u] - l * ee[u];
+            if (fabs(dp) < DBL_MIN) dp = eps_piv;
         }
     }
-    __syncthreads();
-    // Re-orthogonalise clusters of (numerically) equal eigenvalues: MGS by one warp per cluster.
-    const double clus = 1e-10 * tnorm;
-    if (tid < 32) {
-        int k = 0;
-        while (k < r) {
-            int k1 = k + 1;
-            while (k1 < r && fabs(lam[k1 - 1] - lam[k1]) <= clus) ++k1;
-            for (int pass = 0; pass < 2 && k1 - k > 1; ++pass) {
-                for (int j = k; j < k1; ++j) {
-                    for (int i = k; i < j; ++i) {
-                        double dot = 0.0;
-                        for (int t = tid; t < n; t += 32) dot += Z[t * S + i] * Z[t * S + j];
-                        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                        for (int t = tid; t < n; t += 32) Z[t * S + j] -= dot * Z[t * S + i];
-                        __syncwarp();
-                    }
-                    double nn = 0.0;
-                    for (int t = tid; t < n; t += 32) nn += Z[t * S + j] * Z[t * S + j];
-                    for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
-                    const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-                    for (int t = tid; t < n; t += 32) Z[t * S + j] *= inv;
+    for (; i < n - 1; ++i) {
+        W_(i) = dp;
+        const double l = e[i] * rcp_nr(dp);
+        L_(i) = l;
+        dp = (d[i + 1] - lmb) - l * e[i];
+        if (fabs(dp) < DBL_MIN) dp = eps_piv;
+    }
+    W_(n - 1) = dp;
+    // progressive: D-_i = (d_i - lam) - e_i^2 / D-_{i+1}; gamma_i = D+_i + D-_i - (d_i - lam)
+    double dm = d[n - 1] - lmb;
+    if (fabs(dm) < DBL_MIN) dm = eps_piv;
+    int t = n - 1;
+    double best = fabs(dp + dm - (d[n - 1] - lmb));
+    i = n - 2;
+    for (; i >= 3; i -= 4) {
+        double ee[4], dd[4], pp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { ee[u] = e[i - u]; dd[u] = d[i - u] - lmb; pp[u] = W_(i - u); }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double um = ee[u] * rcp_nr(dm);
+            W_(i - u) = um;
+            dm = dd[u] - um * ee[u];
+            if (fabs(dm) < DBL_MIN) dm = eps_piv;
+            const double g = fabs(pp[u] + dm - dd[u]);
+            if (g < best) { best = g; t = i - u; }
+        }
+    }
+    for (; i >= 0; --i) {
+        const double dd = d[i] - lmb, pp = W_(i);
+        const double um = e[i] * rcp_nr(dm);
+        W_(i) = um;
+        dm = dd - um * e[i];
+        if (fabs(dm) < DBL_MIN) dm = eps_piv;
+        const double g = fabs(pp + dm - dd);
+        if (g < best) { best = g; t = i; }
+    }
+    // z: z_t = 1; z_i (i < t) into L_(i), z_{i+1} (i >= t) into W_(i)
+    double s2 = 1.0, z = 1.0;
+    for (i = t - 1; i >= 0; --i) {
+        z = -L_(i) * z;
+        L_(i) = z;
+        s2 += z * z;
+    }
+    z = 1.0;
+    for (i = t; i < n - 1; ++i) {
+        z = -W_(i) * z;
+        W_(i) = z;
+        s2 += z * z;
+    }
+    const double inv = 1.0 / sqrt(s2);
+    const long long S = r;
+    for (i = 0; i < n; ++i) {
+        const double zi = i < t ? L_(i) : (i == t ? 1.0 : W_(i - 1));
+        ed.z[i * S + k] = zi * inv;
+    }
+#undef L_
+#undef W_
+}
+
+// Re-orthogonalise clusters of (numerically) equal eigenvalues: MGS by one warp per factor (clusters are rare;
+// the scan is O(r)).
+__global__ void __launch_bounds__(32) reorth_kernel(const EigDesc* __restrict__ descs) {
+    const EigDesc& ed = descs[blockIdx.x];
+    const int n = ed.n, r = ed.r;
+    __shared__ double d[kMaxN], e[kMaxN], lam[kMaxN], bnd[3];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += 32) {
+        d[i] = ed.dvec[i];
+        e[i] = (i < n - 1) ? ed.evec[i] : 0.0;
+    }
+    for (int i = tid; i < r; i += 32) lam[i] = ed.evals[i];
+    __syncwarp();
+    tri_bounds(d, e, n, bnd);
+    __syncwarp();
+    const double clus = 1e-10 * bnd[2];
+    bool any = false;
+    for (int i = tid + 1; i < r; i += 32) any |= fabs(lam[i - 1] - lam[i]) <= clus;
+    if (!__any_sync(0xffffffffu, any)) return;
+    const long long S = r;
+    double* Z = ed.z;
+    int k = 0;
+    while (k < r) {
+        int k1 = k + 1;
+        while (k1 < r && fabs(lam[k1 - 1] - lam[k1]) <= clus) ++k1;
+        for (int pass = 0; pass < 2 && k1 - k > 1; ++pass) {
+            for (int j = k; j < k1; ++j) {
+                for (int i = k; i < j; ++i) {
+                    double dot = 0.0;
+                    for (int t = tid; t < n; t += 32) dot += Z[t * S + i] * Z[t * S + j];
+                    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                    for (int t = tid; t < n; t += 32) Z[t * S + j] -= dot * Z[t * S + i];
                     __syncwarp();
                 }
+                double nn = 0.0;
+                for (int t = tid; t < n; t += 32) nn += Z[t * S + j] * Z[t * S + j];
+                for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+                const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+                for (int t = tid; t < n; t += 32) Z[t * S + j] *= inv;
+                __syncwarp();
             }
-            k = k1;
         }
+        k = k1;
     }
 }
 
@@ -423,7 +611,17 @@ void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaSt
     k<<<nfactors, 1024, dyn, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
-    tdeig_kernel<<<nfactors, 256, 0, s>>>(d_descs);
+    const unsigned rchunks = (unsigned)std::max<int64_t>(1, ceil_div(std::max(rmax, 1), kBisE));
+    bisect_kernel<<<dim3(rchunks, (unsigned)nfactors), kBisThreads, 0, s>>>(d_descs);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+    const size_t evb = eigvec_smem_bytes(nmax);
+    RKFAC_CUDA(cudaFuncSetAttribute(eigvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)evb));
+    eigvec_kernel<<<dim3((unsigned)ceil_div(std::max(rmax, 1), kVecThreads), (unsigned)nfactors), kVecThreads, evb,
+                    s>>>(d_descs);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+    reorth_kernel<<<nfactors, 32, 0, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
     const size_t bx = (size_t)nmax * kBxCols * 8;
