@@ -9,16 +9,16 @@
 // downstream (C = Q^T X Q and U = Q P are basis independent), so rank-deficient columns -- which the
 // reference skips (qr.hpp:35-45, H = I) -- are replaced here by any unit vector orthogonal to the others.
 //
-// cholinv_kernel: one CTA (1024 threads) per factor.  The lower triangle lives in shared memory in a
+// cholinv_kernel: one CTA (512 threads) per factor.  The lower triangle lives in shared memory in a
 // "padded packed" layout: row i starts at a 16-byte aligned offset and is zero-padded to a multiple of 4 entries,
 // so every inner loop is a 4x4 register tile fed by LDS.128 and the zero padding doubles as the upper-triangle
 // zeros of L^{-1}.  w <= 230 fits in FP64 (w <= 330 in FP32); larger w uses a global scratch.  Latency matters
 // more than the w^3/3 flops, so:
 //   Cholesky   right-looking over 32-wide panels: the 32x32 diagonal block is factored by one warp in registers
-//              (shuffles, no block barrier), the panel below by a row-parallel TRSM, the trailing update by 4x4
-//              register tiles -- 3 barriers per panel;
-//   inverse    all 32x32 diagonal blocks inverted concurrently (one warp each), then block rows
-//              X_I = -(D_I^{-1} L_I,<I) X_<I in place, 4x4 register tiles -- 3 barriers per block row.
+//              (pivot chain on shuffles, the rest of each column software-pipelined through shared memory), the
+//              panel below by a row-parallel TRSM, the trailing update by 4x4 register tiles;
+//   inverse    all 32x32 diagonal blocks inverted concurrently (one warp each), then recursive doubling over block
+//              segments, B <- -C^{-1} B A^{-1}, as passes of register tiles (log2(w/32) levels, 4 barriers each).
 #include <cmath>
 
 #include "kernels.cuh"
@@ -28,6 +28,19 @@ namespace rkfac_b200 {
 namespace {
 
 constexpr int kNB = 32;
+
+// Optional per-phase clock64 stamps (tools/chol_bench.cu builds with -DRKFAC_PHASE_TIMING).
+#ifdef RKFAC_PHASE_TIMING
+__device__ long long g_chol_phase[64 * 64];
+#define CHOL_PHASE(k)                                                                     \
+    do {                                                                                  \
+        const long long t_ = clock64();                                                   \
+        if (threadIdx.x == 0 && blockIdx.x < 64) g_chol_phase[blockIdx.x * 64 + (k)] = t_; \
+        __syncwarp(); /* reconverge warp 0: a split warp would run the shuffles emulated */ \
+    } while (0)
+#else
+#define CHOL_PHASE(k)
+#endif
 constexpr int kMaxW = 512;
 constexpr int kCholThreads = 512;  // 128-register budget: the unrolled 32-wide row arrays stay in registers
 
@@ -60,6 +73,26 @@ __device__ __forceinline__ void ld4(const T* p, T (&v)[4]) {
 
 // kSmem selects the storage of the triangle at compile time: a pointer chosen at run time between shared and
 // global memory compiles to generic LD/ST (measured ~2.5x slower than LDS/STS on this kernel).
+template <class T>
+__device__ __forceinline__ T rsqrt_t(T x);
+template <>
+__device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
+template <>
+__device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
+
+// Lower-triangular tile enumeration of a trapezoid: column tiles [0, CJ), row tiles [J, TR) (column-major):
+// t -> (I, J) with offset(J) = J*TR - J(J-1)/2.
+__device__ __forceinline__ void trap_tile(int t, int TR, int& I, int& J) {
+    // solve J*TR - J(J-1)/2 <= t for the largest J
+    const float b = (float)TR + 0.5f;
+    int j = (int)(b - sqrtf(fmaxf(b * b - 2.f * (float)t, 0.f)));
+    j = max(j, 0);
+    while (j > 0 && j * TR - j * (j - 1) / 2 > t) --j;
+    while ((j + 1) * TR - (j + 1) * j / 2 <= t) ++j;
+    J = j;
+    I = j + (t - (j * TR - j * (j - 1) / 2));
+}
+
 template <class TG, class T, bool kSmem>
 __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* __restrict__ descs, double tol) {
     const CholDesc& cd = descs[blockIdx.x];
@@ -68,77 +101,191 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
     const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // dynamic smem: [small per-factor state][padded packed triangle (kSmem only)]
-    T (*l11t)[kNB + 1] = reinterpret_cast<T (*)[kNB + 1]>(smem_raw);          // transposed diagonal block
-    T* dinv = reinterpret_cast<T*>(smem_raw + sizeof(T) * kNB * (kNB + 1));    // its reciprocal diagonal
-    float* diag0 = reinterpret_cast<float*>(dinv + kNB);                       // original diagonal of G
-    unsigned char* defic = reinterpret_cast<unsigned char*>(diag0 + rup4(n));  // rank-deficiency flags
+    T* colbuf = reinterpret_cast<T*>(smem_raw);                                   // column broadcast (warp 0)
+    T* dinv = colbuf + 2 * kNB;                                                    // reciprocal diagonal of L_bb
+    float* diag0 = reinterpret_cast<float*>(smem_raw + sizeof(T) * (kNB * (kNB + 1) + kNB));  // diag of G
+    unsigned char* defic = reinterpret_cast<unsigned char*>(diag0 + rup4(n));    // rank-deficiency flags
     __shared__ int any_defic;
     T* L;
     if constexpr (kSmem) L = reinterpret_cast<T*>(smem_raw + cholinv_state_bytes(n, sizeof(T)));
     else L = static_cast<T*>(cd.scratch);
     const T tolT = T(tol);
 
+    CHOL_PHASE(0);
+    // Lower triangle of G (the Gram matrix is symmetric; its upper half is not read).  Same element type and a
+    // 16-byte aligned pitch: asynchronous 16-byte copies straight into the packed rows (all in flight at once),
+    // then the few upper entries a copy brought into the zero padding are cleared.
     const TG* G = static_cast<const TG*>(cd.G);
-    for (int i = warp; i < n; i += nwarp) {
-        T* row = L + prow(i);
-        for (int j = lane; j < rup4(i + 1); j += 32)
-            row[j] = (j <= i) ? T(0.5) * (T(G[(long long)i * cd.ldg + j]) + T(G[(long long)j * cd.ldg + i])) : T(0);
+    bool async_load = false;
+    if constexpr (kSmem && sizeof(TG) == sizeof(T)) {
+        async_load = ((cd.ldg * (long long)sizeof(T)) & 15) == 0 && (((uintptr_t)G) & 15) == 0 && cd.ldg >= rup4(n);
+        if (async_load) {
+            constexpr int E = 16 / sizeof(T);
+            for (int i = warp; i < n; i += nwarp) {
+                const int nch = rup4(i + 1) / E;
+                for (int c = lane; c < nch; c += 32) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(L + prow(i) + c * E);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                                 "l"(G + (long long)i * cd.ldg + c * E));
+                }
+            }
+            asm volatile("cp.async.wait_all;\n" ::);
+            __syncthreads();
+            for (int i = tid; i < n; i += nthr)
+                for (int j = i + 1; j < rup4(i + 1); ++j) L[prow(i) + j] = T(0);
+        }
+    }
+    if (!async_load) {
+        for (int i = warp; i < n; i += nwarp) {
+            T* row = L + prow(i);
+            for (int j = lane; j < rup4(i + 1); j += 32) row[j] = (j <= i) ? T(G[(long long)i * cd.ldg + j]) : T(0);
+        }
     }
     for (int i = tid; i < n; i += nthr) defic[i] = 0;
     if (tid == 0) any_defic = 0;
     __syncthreads();
     for (int i = tid; i < n; i += nthr) diag0[i] = (float)L[prow(i) + i];
     __syncthreads();
+    CHOL_PHASE(1);
 
     const int nblk = (n + kNB - 1) / kNB;
-    // ------------------------------------------------------------------ blocked right-looking Cholesky
-    for (int b = 0; b < nblk; ++b) {
+
+    // 32x32 diagonal block b, one warp, lane = row, right-looking: the pivot is read by shuffle, the scaled column
+    // is broadcast through shared memory.  Deficient pivots (<= tol * G_kk) give L_kk = 1 and a zero column.
+    auto factor_diag = [&](int b) {
         const int J0 = b * kNB, nb = min(kNB, n - J0);
-        if (warp == 0) {
-            // (1) 32x32 diagonal block in registers, lane i owns row J0+i.  Step k broadcasts column k by
-            //     shuffles issued in batches of 8 before their FMAs (a SHFL->FFMA chain per element serialises on
-            //     the shuffle latency).
-            T a[kNB];
-            const T* rowp = L + prow(J0 + min(lane, nb - 1)) + J0;
+        T a[kNB];
+        const int rl = min(lane, nb - 1);
+        const T* rowp = L + prow(J0 + rl) + J0;
 #pragma unroll
-            for (int c = 0; c < kNB; ++c) a[c] = (lane < nb && c <= lane) ? rowp[c] : T(0);
+        for (int c4 = 0; c4 < kNB; c4 += 4) {
+            T v4[4] = {T(0), T(0), T(0), T(0)};
+            if (c4 <= rl) ld4(rowp + c4, v4);  // row J0+rl holds rup4(J0+rl+1) >= J0+c4+4 entries
 #pragma unroll
-            for (int k = 0; k < kNB; ++k) {
-                if (k < nb) {
-                    const T piv = __shfl_sync(0xffffffffu, a[k], k);
-                    const T g = T(diag0[J0 + k]);
-                    const bool def = !(piv > tolT * g) || g == T(0);
-                    const T lkk = def ? T(1) : sqrt(piv);
-                    const T inv = def ? T(0) : T(1) / lkk;
-                    if (lane == k) {
-                        a[k] = lkk;
-                        dinv[k] = inv;
-                        if (def) { defic[J0 + k] = 1; any_defic = 1; }
-                    } else if (lane > k) {
-                        a[k] *= inv;
+            for (int u = 0; u < 4; ++u) a[c4 + u] = (lane < nb && c4 + u <= lane) ? v4[u] : T(0);
+        }
+        // Lanes above the diagonal only touch their (never stored) upper part, so loads and FMAs need no per-lane
+        // predicate (a predicated load would put its latency on the chain of every update).  Step k's pivot is
+        // read by shuffle; the entry the next pivot depends on, L(k+1, k), is shuffled too and applied first,
+        // while the rest of column k goes through shared memory and is applied one step later (FP32: software
+        // pipelined, so the shared-memory round trip leaves the pivot chain).
+        T tp[kNB];  // column k-1, entries j >= k+1 (pipelined remainder)
+        auto step = [&](int k, int nbv, bool defer) {
+            const T piv = __shfl_sync(0xffffffffu, a[k], k);
+            const T g = T(diag0[J0 + k]);
+            const bool def = !(piv > tolT * g) || g == T(0);
+            const T inv = def ? T(0) : rsqrt_t(piv);
+            const T lkk = def ? T(1) : piv * inv;
+            a[k] = lane == k ? lkk : (lane > k ? a[k] * inv : a[k]);
+            if (lane == 0) dinv[k] = inv;
+            if (def && lane == 0) { defic[J0 + k] = 1; any_defic = 1; }
+            if (k + 1 < nbv) {
+                const T tn = __shfl_sync(0xffffffffu, a[k], k + 1);
+                T* cb = colbuf + (k & 1) * kNB;  // double-buffered: one __syncwarp per step
+                cb[lane] = a[k];
+                __syncwarp();
+                if (defer) {
+                    T tc[kNB];
+#pragma unroll
+                    for (int q4 = (k + 2) & ~3; q4 < kNB; q4 += 4) {
+                        T v4[4];
+                        ld4(cb + q4, v4);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) tc[q4 + u] = v4[u];
                     }
+                    if (k >= 1) {  // remainder of column k-1 (j >= k+1), loaded one step ago
 #pragma unroll
-                    for (int j0 = k + 1; j0 < kNB; j0 += 8) {
-                        T t[8];
+                        for (int j = k + 1; j < kNB; ++j) a[j] -= a[k - 1] * tp[j];
+                    }
+                    a[k + 1] -= a[k] * tn;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (j0 + u < kNB) t[u] = __shfl_sync(0xffffffffu, a[k], j0 + u);
+                    for (int j = k + 2; j < kNB; ++j) tp[j] = tc[j];
+                } else {
+                    a[k + 1] -= a[k] * tn;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (j0 + u < kNB && lane >= j0 + u) a[j0 + u] -= a[k] * t[u];
+                    for (int q4 = (k + 2) & ~3; q4 < kNB; q4 += 4) {
+                        T v4[4];
+                        ld4(cb + q4, v4);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (q4 + u >= k + 2) a[q4 + u] -= a[k] * v4[u];
                     }
                 }
-            }
-            if (lane < nb) {
-                T* wrow = L + prow(J0 + lane) + J0;
+            } else if (defer && k >= 1) {
 #pragma unroll
-                for (int c = 0; c < kNB; ++c)
-                    if (c <= lane) wrow[c] = a[c];
+                for (int j = k + 1; j < kNB; ++j) a[j] -= a[k - 1] * tp[j];
+            }
+        };
+        constexpr bool kDefer = sizeof(T) == 4;  // FP64: the second column buffer would exceed the register budget
+        if (nb == kNB) {
+#pragma unroll
+            for (int k = 0; k < kNB; ++k) step(k, kNB, kDefer);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kNB; ++k)
+                if (k < nb) step(k, nb, false);
+        }
+        if (lane < nb) {
+            T* wrow = L + prow(J0 + lane) + J0;
+#pragma unroll
+            for (int c = 0; c < kNB; ++c)
+                if (c <= lane) wrow[c] = a[c];
+        }
+    };
+
+    // Trailing update A(i, j) -= sum_c L(i, J0+c) L(j, J0+c) over the lower trapezoid with columns [c0, c1) and
+    // rows [c0, n), 4x4 register tiles (LDS.128 along the panel), tiles spread over threads [t0, t0 + nt).
+    auto update = [&](int J0, int nb, int c0, int c1, int t0, int nt) {
+        if (c0 >= c1 || tid < t0 || tid >= t0 + nt) return;
+        const int TR = (n - c0 + 3) / 4, CJ = (c1 - c0 + 3) / 4;
+        const int ntiles = CJ * TR - CJ * (CJ - 1) / 2;
+        for (int t = tid - t0; t < ntiles; t += nt) {
+            int I, J;
+            trap_tile(t, TR, I, J);
+            const T* ra[4];
+            const T* rb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ra[u] = L + prow(min(c0 + I * 4 + u, n - 1)) + J0;
+                rb[u] = L + prow(min(c0 + J * 4 + u, n - 1)) + J0;
+            }
+            T acc[4][4] = {};
+#pragma unroll
+            for (int c4 = 0; c4 < kNB; c4 += 4) {
+                if (c4 < nb) {
+                    T av[4][4], bv[4][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { ld4(ra[u] + c4, av[u]); ld4(rb[u] + c4, bv[u]); }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c4 + c < nb)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                for (int v = 0; v < 4; ++v) acc[u][v] += av[u][c] * bv[v][c];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int ii = c0 + I * 4 + u;
+                if (ii >= n) continue;
+                T* wr = L + prow(ii);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int jj = c0 + J * 4 + v;
+                    if (jj <= ii && jj < c1) wr[jj] -= acc[u][v];
+                }
             }
         }
-        __syncthreads();
-        // (2) panel TRSM (left-looking per row, 4 partial sums per dot, reciprocal diagonal); rows below the
-        //     block, one thread per row; L11 rows are broadcast from smem.  Deficient columns give 0.
+    };
+
+    // ------------------------------------------------------------------ Cholesky, right-looking with look-ahead
+    if (warp == 0) factor_diag(0);
+    __syncthreads();
+    CHOL_PHASE(2);
+    for (int b = 0; b < nblk; ++b) {
+        const int J0 = b * kNB, nb = min(kNB, n - J0);
+        // panel TRSM: rows below the block, one thread per row, forward substitution with 4 partial sums
         const int rows = n - J0 - nb;
         for (int t = tid; t < rows; t += nthr) {
             const int i = J0 + nb + t;
@@ -158,10 +305,12 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
                     T s0 = x[c], s1 = T(0), s2 = T(0), s3 = T(0);
 #pragma unroll
                     for (int q = 0; q < c; q += 4) {
-                        s0 -= x[q] * lc[q];
-                        if (q + 1 < c) s1 -= x[q + 1] * lc[q + 1];
-                        if (q + 2 < c) s2 -= x[q + 2] * lc[q + 2];
-                        if (q + 3 < c) s3 -= x[q + 3] * lc[q + 3];
+                        T l4[4];
+                        ld4(lc + q, l4);
+                        s0 -= x[q] * l4[0];
+                        if (q + 1 < c) s1 -= x[q + 1] * l4[1];
+                        if (q + 2 < c) s2 -= x[q + 2] * l4[2];
+                        if (q + 3 < c) s3 -= x[q + 3] * l4[3];
                     }
                     x[c] = ((s0 + s1) + (s2 + s3)) * dinv[c];
                 }
@@ -171,53 +320,18 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
                 if (c < nb) rp[c] = x[c];
         }
         __syncthreads();
-        // (3) trailing update A22 -= L21 L21^T (lower triangle), 4x4 tiles, LDS.128 along the panel columns
-        const int t0 = J0 + nb, m = n - t0;
-        if (m > 0) {
-            const int TI = (m + 3) / 4;
-            const int ntiles = TI * (TI + 1) / 2;
-            for (int t = tid; t < ntiles; t += nthr) {
-                int I = (int)((sqrtf(8.f * (float)t + 1.f) - 1.f) * 0.5f);
-                while (I * (I + 1) / 2 > t) --I;
-                while ((I + 1) * (I + 2) / 2 <= t) ++I;
-                const int J = t - I * (I + 1) / 2;
-                const T* ra[4];
-                const T* rb[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    ra[u] = L + prow(min(t0 + I * 4 + u, n - 1)) + J0;
-                    rb[u] = L + prow(min(t0 + J * 4 + u, n - 1)) + J0;
-                }
-                T acc[4][4] = {};
-#pragma unroll
-                for (int c4 = 0; c4 < kNB; c4 += 4) {
-                    if (c4 < nb) {  // panel columns beyond nb are zero padding / next rows: masked below
-                        T av[4][4], bv[4][4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) { ld4(ra[u] + c4, av[u]); ld4(rb[u] + c4, bv[u]); }
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (c4 + c < nb)
-#pragma unroll
-                                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                                    for (int v = 0; v < 4; ++v) acc[u][v] += av[u][c] * bv[v][c];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int ii = t0 + I * 4 + u;
-                    if (ii >= n) continue;
-                    T* wr = L + prow(ii);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int jj = t0 + J * 4 + v;
-                        if (jj <= ii) wr[jj] -= acc[u][v];
-                    }
-                }
-            }
+        CHOL_PHASE(3 + 3 * b);
+        if (b + 1 < nblk) {
+            // trailing update of everything right of the panel (all warps), then the next diagonal block (warp 0;
+            // overlapping it with the update was measured slower: the update's shared-memory traffic stalls the
+            // factorisation's latency-bound chain)
+            update(J0, nb, J0 + kNB, n, 0, nthr);
+            __syncthreads();
+            CHOL_PHASE(4 + 3 * b);
+            if (warp == 0) factor_diag(b + 1);
+            __syncthreads();
+            CHOL_PHASE(5 + 3 * b);
         }
-        __syncthreads();
     }
 
     // ------------------------------------------------------------------ triangular inverse, in place
@@ -231,13 +345,18 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
             if (i < nb) {
                 const T* li = L + prow(J0 + i) + J0;
                 const T di = defic[J0 + i] ? T(1) : T(1) / li[i];
-                T s0 = T(0), s1 = T(0);
+                // x[k] = 0 for k < j, so the sums need no predicate (and the loads no per-lane condition)
+                T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
 #pragma unroll
-                for (int k = 0; k < i; k += 2) {
-                    if (k >= j) s0 += li[k] * x[k];
-                    if (k + 1 < i && k + 1 >= j) s1 += li[k + 1] * x[k + 1];
+                for (int k = 0; k < i; k += 4) {
+                    T l4[4];
+                    ld4(li + k, l4);
+                    s0 += l4[0] * x[k];
+                    if (k + 1 < i) s1 += l4[1] * x[k + 1];
+                    if (k + 2 < i) s2 += l4[2] * x[k + 2];
+                    if (k + 3 < i) s3 += l4[3] * x[k + 3];
                 }
-                x[i] = (i < j) ? T(0) : (i == j ? di : -(s0 + s1) * di);
+                x[i] = (i < j) ? T(0) : (i == j ? di : -((s0 + s1) + (s2 + s3)) * di);
             } else {
                 x[i] = T(0);
             }
@@ -250,96 +369,141 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
         }
     }
     __syncthreads();
-    // (b) block rows I = 1..nblk-1: X_I,<i0 = -(D_I^{-1} L_I,<i0) X_<i0,<i0
-    for (int I = 1; I < nblk; ++I) {
-        const int i0 = I * kNB, nbI = min(kNB, n - i0);
-        // step 1 (in place): B = D_I^{-1} L_I,<i0, one thread per column c < i0 (D_I entries broadcast)
-        for (int c = tid; c < i0; c += nthr) {
-            T col[kNB];
-#pragma unroll
-            for (int s = 0; s < kNB; ++s) col[s] = (s < nbI) ? L[prow(i0 + s) + c] : T(0);
-#pragma unroll
-            for (int r = kNB - 1; r >= 0; --r) {  // descending r: col[s] for s <= r is still the input
-                if (r < nbI) {
-                    const T* dr = L + prow(i0 + r) + i0;
-                    T acc = T(0);
-#pragma unroll
-                    for (int s = 0; s <= r; ++s) acc += dr[s] * col[s];
-                    col[r] = acc;
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < kNB; ++r)
-                if (r < nbI) L[prow(i0 + r) + c] = col[r];
+    CHOL_PHASE(51);
+    // (b) recursive doubling over block segments: for [A 0; B C] with A^-1, C^-1 in place,
+    //     B <- -C^-1 (B A^-1).  Both products run as passes of 4x4 tiles held in registers (all reads of a pass
+    //     precede its writes); product 1 goes by increasing column (T_ij reads B_ik, k >= j), product 2 by
+    //     decreasing row (R_ij reads T_kj, k <= i), so no pass overwrites what a later pass reads.
+    for (int s = 1; s < nblk; s *= 2) {
+        const int nseg = (nblk + 2 * s - 1) / (2 * s);
+        // tiles per segment: rows of C x columns of A (in 4-tiles)
+        int total = 0;
+        for (int g = 0; g < nseg; ++g) {
+            const int cs = (2 * g + 1) * s * kNB, ce = min((2 * g + 2) * s * kNB, n);
+            if (cs < n) total += ((ce - cs + 3) / 4) * (s * kNB / 4);
         }
-        __syncthreads();
-        // step 2: X(i0+r, c) = -sum_{k=c}^{i0-1} B(r, k) X(k, c); 4x4 tiles; X rows are zero-padded past the
-        // diagonal, so whole LDS.128 groups can be used from k = c0 on
-        // Tiles are processed in passes of increasing column c0: a tile reads B(r, k) only for k >= c0 and writes
-        // columns c0..c0+3, so writing a pass in place never clobbers what a later pass still has to read.
-        const int rg = (nbI + 3) / 4, cgs = i0 / 4;
-        const int ntl = rg * cgs;
-        for (int pass = 0; pass * nthr < ntl; ++pass) {
-        const int tt = pass * nthr + tid;
-        T res[4][4];
-        int r0 = 0, c0 = 0;
-        const bool have = tt < ntl;
-        if (have) {
-            r0 = (tt % rg) * 4;
-            c0 = (tt / rg) * 4;
-            const T* rb[4];
+        for (int prod = 0; prod < 2; ++prod) {
+            for (int base = 0; base < total; base += nthr) {
+                const int t = base + tid;
+                T acc[4][4] = {};
+                int r0 = 0, c0 = 0;
+                bool have = false;
+                if (t < total) {
+                    // locate the segment
+                    int g = 0, rem = t, RT = 0, CT = s * kNB / 4, cs = 0, as = 0, ae = 0;
+                    for (;; ++g) {
+                        cs = (2 * g + 1) * s * kNB;
+                        const int ce = min((2 * g + 2) * s * kNB, n);
+                        RT = (ce - cs + 3) / 4;
+                        if (rem < RT * CT) break;
+                        rem -= RT * CT;
+                    }
+                    as = 2 * g * s * kNB;
+                    ae = cs;
+                    int rt, ct;
+                    if (prod == 0) { ct = rem / RT; rt = rem - ct * RT; }                // column-major, increasing c
+                    else { const int q = rem / CT; ct = rem - q * CT; rt = RT - 1 - q; }  // row-major, decreasing r
+                    r0 = cs + rt * 4;
+                    c0 = as + ct * 4;
+                    have = true;
+                    const T* rr[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) rb[u] = L + prow(i0 + min(r0 + u, nbI - 1));
-            T acc[4][4] = {};
-            for (int k4 = c0; k4 < i0; k4 += 4) {
-                T bv[4][4], xv[4][4];
+                    for (int u = 0; u < 4; ++u) rr[u] = L + prow(min(r0 + u, n - 1));
+                    if (prod == 0) {
+                        // T(r, c) = sum_{k=c}^{ae-1} B(r, k) Ainv(k, c)
+                        for (int k4 = c0; k4 < ae; k4 += 4) {
+                            T bv[4][4], xv[4][4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) ld4(rb[u] + k4, bv[u]);
+                            for (int u = 0; u < 4; ++u) ld4(rr[u] + k4, bv[u]);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) ld4(L + prow(k4 + kk) + c0, xv[kk]);
+                            for (int kk = 0; kk < 4; ++kk) ld4(L + prow(k4 + kk) + c0, xv[kk]);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
+                            for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) acc[u][v] += bv[u][kk] * xv[kk][v];
+                        }
+                    } else {
+                        // R(r, c) = -sum_{k=cs}^{r} Cinv(r, k) T(k, c)  (Cinv zero-padded past the diagonal)
+                        const int kend = min(r0 + 4, n);
+                        for (int k4 = cs; k4 < kend; k4 += 4) {
+                            T cv[4][4], xv[4][4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) ld4(rr[u] + k4, cv[u]);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) ld4(L + prow(min(k4 + kk, n - 1)) + c0, xv[kk]);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                if (k4 + kk < n)
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                        for (int v = 0; v < 4; ++v) acc[u][v] -= cv[u][kk] * xv[kk][v];
+                        }
+                    }
+                }
+                __syncthreads();
+                if (have) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
+                        if (r0 + u < n) {
+                            T* wr = L + prow(r0 + u) + c0;
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) acc[u][v] += bv[u][kk] * xv[kk][v];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) res[u][v] = -acc[u][v];
-        }
-        __syncthreads();
-        if (have) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (r0 + u < nbI) {
-                    T* wr = L + prow(i0 + r0 + u) + c0;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) wr[v] = res[u][v];
+                            for (int v = 0; v < 4; ++v) wr[v] = acc[u][v];
+                        }
                 }
+                __syncthreads();
+            }
         }
-        __syncthreads();
-        }  // pass
     }
 
+    CHOL_PHASE(56);
     // ------------------------------------------------------------------ outputs
+    // Only the lower triangle (and its zero padding to a multiple of 4) is stored, 4 elements per thread: the
+    // strictly upper part of Linv / Linv_lo is zero from the workspace's creation and never written.
     T* out = static_cast<T*>(cd.Linv);
     float* lo = static_cast<float*>(cd.Linv_lo);
-    const int wcols = (int)min((long long)rup4(n), cd.ldl);
+    const bool vec_out = (cd.ldl & 3) == 0 && (((uintptr_t)out) & (4 * sizeof(T) - 1)) == 0 &&
+                         (!lo || (((uintptr_t)lo) & 15) == 0);
     for (int i = warp; i < n; i += nwarp) {
         const T* row = L + prow(i);
-        for (int j = lane; j < wcols; j += 32) {
-            const T v = (j <= i && !defic[i]) ? row[j] : T(0);
-            out[(long long)i * cd.ldl + j] = v;
-            if (lo) {
-                const float f = (float)v;
-                lo[(long long)i * cd.ldl + j] = f - tf32_trunc(f);
+        const bool z = defic[i];
+        const int len = min(rup4(i + 1), (int)cd.ldl);
+        if (vec_out) {
+            for (int c = lane * 4; c < len; c += 128) {
+                T v[4];
+                ld4(row + c, v);
+                if (z) v[0] = v[1] = v[2] = v[3] = T(0);
+                T* o = out + (long long)i * cd.ldl + c;
+                if constexpr (sizeof(T) == 4) {
+                    *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+                } else {
+                    reinterpret_cast<double2*>(o)[0] = make_double2(v[0], v[1]);
+                    reinterpret_cast<double2*>(o)[1] = make_double2(v[2], v[3]);
+                }
+                if (lo) {
+                    float f[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { const float x = (float)v[u]; f[u] = x - tf32_trunc(x); }
+                    *reinterpret_cast<float4*>(lo + (long long)i * cd.ldl + c) = make_float4(f[0], f[1], f[2], f[3]);
+                }
+            }
+        } else {
+            for (int j = lane; j < len; j += 32) {
+                const T v = z ? T(0) : row[j];
+                out[(long long)i * cd.ldl + j] = v;
+                if (lo) {
+                    const float f = (float)v;
+                    lo[(long long)i * cd.ldl + j] = f - tf32_trunc(f);
+                }
             }
         }
     }
     for (int i = tid; i < n; i += nthr) cd.flags[i] = defic[i];
     if (tid == 0) *cd.nflags = any_defic;
+    __syncthreads();
+    CHOL_PHASE(57);
 }
 
 // Deterministic pseudo-random candidate for completing a rank-deficient column.

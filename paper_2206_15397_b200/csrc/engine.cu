@@ -89,7 +89,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         }
         o.Xc = c.take<float>(d * dp);
         o.Xl = c.take<float>(d * dp);
-        o.G64 = c.take<double>(w * w);
+        o.G64 = c.take<double>(w * wp);
         o.G32 = c.take<float>(w * wp);
         o.L64 = c.take<double>(w * wp);
         o.L32 = c.take<float>(w * wp);
@@ -321,7 +321,7 @@ void Plan::build_decomp_stages() {
                 tri_[dir]->add(t);
             }
             // FP64 CholeskyQR of Y into Q (DMMA): G = Y^T Y in FP64, Q^T = Linv Y^T with FP64 accumulation
-            gram64_[dir]->add(F.w, F.d, Y.T, F.dp, F.G64, F.w);
+            gram64_[dir]->add(F.w, F.d, Y.T, F.dp, F.G64, F.wp);
             tri64_[dir]->add(F.w, F.d, F.Linv64, F.wp, Y.T, F.dp, Q.T, Q.Tlo, F.dp);
             comp.push_back(CompleteDesc{F.w, F.d, F.dp, Q.T, F.flags, F.flags + F.w, Q.Tlo, Q.R, Q.Rlo, F.wp});
             // core: srevd C = Q^T (X Q) (rnla.hpp:97); rsvd_psd B B^T = Y^T Y (eig.hpp:251)
@@ -367,7 +367,7 @@ void Plan::build_decomp_stages() {
     std::vector<CompleteDesc> cu;
     std::vector<BracketDesc> br;
     for (auto& F : f_) {
-        c64.push_back(CholDesc{F.w, F.G64, F.w, F.Linv64, F.wp, nullptr, F.flags, F.flags + F.w, F.chol_scratch});
+        c64.push_back(CholDesc{F.w, F.G64, F.wp, F.Linv64, F.wp, nullptr, F.flags, F.flags + F.w, F.chol_scratch});
         c32.push_back(CholDesc{F.w, F.G32, F.wp, F.Linv32, F.wp, F.Linv32lo, F.flags, F.flags + F.w, F.chol_scratch});
         EigDesc e{};
         e.n = F.w; e.r = F.r; e.A = F.core; e.lda = F.w; e.scratch = F.eig_scratch; e.refl = F.refl;
