@@ -373,12 +373,12 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 uint32_t r[32];
                 tmem_ld32(tbase + c0, r);
                 const int nbase = tl.n0 + c0;
-                if (pr.ksplit > 1) {
+                if (pr.ksplit > 1) {  // raw partials, column-major per slice: each store is 128 B across the warp
                     if (m < pr.M) {
-                        float* part = pr.partial + (long long)tl.slice * pr.M * pr.N + (long long)m * pr.N;
+                        float* part = pr.partial + ((long long)tl.slice * pr.N + nbase) * pr.M + m;
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (nbase + j < nlim) part[nbase + j] = __uint_as_float(r[j]);
+                            if (nbase + j < nlim) part[(long long)j * pr.M] = __uint_as_float(r[j]);
                     }
                     continue;
                 }
@@ -428,19 +428,31 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     }
 }
 
-// Deterministic split-K reduction (fixed slice order) + the full epilogue.
-__global__ void tc_reduce_kernel(const TcProb* __restrict__ probs, int nprob) {
-    for (int p = 0; p < nprob; ++p) {
-        const TcProb& pr = probs[p];
-        if (pr.ksplit <= 1) continue;
-        const long long mn = (long long)pr.M * pr.N;
-        for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mn;
-             e += (long long)gridDim.x * blockDim.x) {
-            float s = pr.partial[e];
-            for (int k = 1; k < pr.ksplit; ++k) s += pr.partial[(long long)k * mn + e];
-            const int m = (int)(e / pr.N), n = (int)(e - (long long)m * pr.N);
-            store_outputs(pr, m, n, epi_value(pr, m, n, s));
+// Deterministic split-K reduction (fixed slice order) + the full epilogue, flattened over every split problem's
+// elements (one pass; the slices of an element are loaded 4 at a time).
+__global__ void tc_reduce_kernel(const TcProb* __restrict__ probs, const TcRed* __restrict__ red, int nred,
+                                 long long total) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nred - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (red[mid].off <= e) lo = mid; else hi = mid - 1;
         }
+        const TcProb& pr = probs[red[lo].prob];
+        const long long local = e - red[lo].off;
+        const long long mn = (long long)pr.M * pr.N;
+        const float* part = pr.partial + local;
+        float s0 = part[0], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int k = 1;
+        for (; k + 3 < pr.ksplit; k += 4) {  // fixed association: ((s0 + s1) + (s2 + s3)) per group of 4
+            const float a = part[k * mn], b = part[(k + 1) * mn], c = part[(k + 2) * mn], d = part[(k + 3) * mn];
+            s0 += a; s1 += b; s2 += c; s3 += d;
+        }
+        for (; k < pr.ksplit; ++k) s0 += part[k * mn];
+        const float s = (s0 + s1) + (s2 + s3);
+        const int n = (int)(local / pr.M), m = (int)(local - (long long)n * pr.M);  // partials are column-major
+        store_outputs(pr, m, n, epi_value(pr, m, n, s));
     }
 }
 
@@ -549,12 +561,19 @@ void TcGemm::finalize() {
     partials_.alloc(std::max<size_t>(total, 1) * sizeof(float));
     size_t off = 0;
     any_split_ = false;
-    for (auto& p : probs_)
+    std::vector<TcRed> red;
+    red_total_ = 0;
+    for (size_t i = 0; i < probs_.size(); ++i) {
+        TcProb& p = probs_[i];
         if (p.ksplit > 1) {
             p.partial = partials_.as<float>() + off;
             off += (size_t)p.ksplit * p.M * p.N;
             any_split_ = true;
+            red.push_back(TcRed{red_total_, (int)i});
+            red_total_ += (long long)p.M * p.N;
         }
+    }
+    nred_ = (int)red.size();
     // LPT over persistent CTAs: tile cost ~ K blocks * (n_tile + epilogue overhead)
     const int ntiles = (int)tiles_.size();
     nctas_ = std::max(1, std::min(ntiles, kNumSMs));
@@ -587,6 +606,7 @@ void TcGemm::finalize() {
     up(d_maps_, maps_.data(), sizeof(CUtensorMap) * maps_.size());
     up(d_tiles_, sched.data(), sizeof(TcTile) * sched.size());
     up(d_begin_, begin.data(), sizeof(int) * begin.size());
+    up(d_red_, red.data(), sizeof(TcRed) * red.size());
 }
 
 size_t TcGemm::smem_bytes() { return (size_t)kStages * kStageBytes + kBarrierBytes + kStageTileBytes + 1024; }
@@ -600,7 +620,8 @@ void TcGemm::launch(cudaStream_t s) const {
     count_launch();
     RKFAC_CHECK_LAUNCH();
     if (any_split_) {
-        tc_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_probs_.as<TcProb>(), (int)probs_.size());
+        const int blocks = (int)std::min<long long>(ceil_div(red_total_, 256), kNumSMs * 8);
+        tc_reduce_kernel<<<blocks, 256, 0, s>>>(d_probs_.as<TcProb>(), d_red_.as<TcRed>(), nred_, red_total_);
         count_launch();
         RKFAC_CHECK_LAUNCH();
     }

@@ -51,6 +51,11 @@ struct TcTile {
     int prob, m0, n0, kb0, kb1, slice, pad_[2];
 };
 
+struct TcRed {  // split-K reduction map: element offset of a split problem in the flattened reduction
+    long long off;
+    int prob;
+};
+
 class TcGemm {
   public:
     int add(const TcProblemDesc& d);
@@ -67,7 +72,9 @@ class TcGemm {
     std::vector<size_t> partial_off_;
     int nctas_ = 0;
     bool any_split_ = false;
-    DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_;
+    int nred_ = 0;
+    long long red_total_ = 0;
+    DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_, d_red_;
 };
 
 // TF32 lo plane (and optional padded copy) of row-major matrices, all problems in one launch.
