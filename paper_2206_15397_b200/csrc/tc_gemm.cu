@@ -256,6 +256,93 @@ __device__ __forceinline__ void chunk_store(const float (&v)[32], float* p, long
     }
 }
 
+// A value plane and its TF32 lo plane in the same layout, written in one pass (the common output pair of the
+// path: the operands of the next tensor-core product).  Interior chunks take pointer-increment fast paths: a
+// transposed chunk is 32 coalesced 128-byte stores per plane, a row-major chunk is staged once through the smem
+// tile and leaves as 128-bit stores of both planes.
+__device__ __forceinline__ float4 lo4(float4 q) {
+    return make_float4(q.x - tf32_trunc(q.x), q.y - tf32_trunc(q.y), q.z - tf32_trunc(q.z), q.w - tf32_trunc(q.w));
+}
+
+__device__ __forceinline__ void chunk_store_pair(const float (&v)[32], float* ph, float* pl, long long ld, int t,
+                                                 int mbase, int nbase, int M, int N, bool skip_lower, bool mirror,
+                                                 float (*tile)[kTP], int lane) {
+    const int m = mbase + lane;
+    if (t) {
+        if (!skip_lower && nbase + 32 <= N) {
+            if (m < M) {
+                float* qh = ph + (long long)nbase * ld + m;
+                float* ql = pl + (long long)nbase * ld + m;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    *qh = v[j];
+                    *ql = v[j] - tf32_trunc(v[j]);
+                    qh += ld;
+                    ql += ld;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int n = nbase + j;
+                if (m < M && n < N && !(skip_lower && n < m)) {
+                    ph[(long long)n * ld + m] = v[j];
+                    pl[(long long)n * ld + m] = v[j] - tf32_trunc(v[j]);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j4 = 0; j4 < 32; j4 += 4)
+            *reinterpret_cast<float4*>(&tile[lane][j4]) = make_float4(v[j4], v[j4 + 1], v[j4 + 2], v[j4 + 3]);
+        __syncwarp();
+        const int c = (lane & 7) * 4;
+        const bool vec = ((reinterpret_cast<uintptr_t>(ph) | reinterpret_cast<uintptr_t>(pl) | (uintptr_t)(ld * 4)) &
+                          15) == 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int mm = mbase + i * 4 + (lane >> 3), n = nbase + c;
+            const float4 q = *reinterpret_cast<const float4*>(&tile[i * 4 + (lane >> 3)][c]);
+            if (vec && mm < M && n + 3 < N && !(skip_lower && n < mm)) {
+                *reinterpret_cast<float4*>(ph + (long long)mm * ld + n) = q;
+                *reinterpret_cast<float4*>(pl + (long long)mm * ld + n) = lo4(q);
+            } else {
+                const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (mm < M && n + u < N && !(skip_lower && n + u < mm)) {
+                        ph[(long long)mm * ld + n + u] = e[u];
+                        pl[(long long)mm * ld + n + u] = e[u] - tf32_trunc(e[u]);
+                    }
+            }
+        }
+        __syncwarp();
+    }
+    if (mirror && m < M) {  // element (n, m) in the opposite layout of the direct store: coalesced when t == 0
+        if (!t && nbase > m + 0 && nbase + 32 <= N) {  // whole chunk strictly above this row's diagonal
+            float* qh = ph + (long long)nbase * ld + m;
+            float* ql = pl + (long long)nbase * ld + m;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                *qh = v[j];
+                *ql = v[j] - tf32_trunc(v[j]);
+                qh += ld;
+                ql += ld;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int n = nbase + j;
+                if (n < N && n > m) {
+                    const long long i = t ? (long long)m * ld + n : (long long)n * ld + m;
+                    ph[i] = v[j];
+                    pl[i] = v[j] - tf32_trunc(v[j]);
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__ maps,
@@ -412,10 +499,21 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     for (int j = 0; j < 32; ++j) v[j] = fmaf(pr.gamma, dv[j], v[j]);
                 }
 #pragma unroll 1
-                for (int o = 0; o < 4; ++o)
-                    if (pr.o[o])
-                        chunk_store(v, pr.o[o], pr.ldo[o], pr.to[o], pr.is_lo[o] != 0, mbase, nbase, pr.M, nlim,
-                                    diag, pr.sym != 0, tile, lane);
+                for (int o = 0; o < 2; ++o) {  // (value, lo) plane pairs 0/2 and 1/3
+                    float* ph = pr.o[o];
+                    float* pl = pr.o[o + 2];
+                    if (ph && pl && pr.to[o] == pr.to[o + 2] && pr.ldo[o] == pr.ldo[o + 2]) {
+                        chunk_store_pair(v, ph, pl, pr.ldo[o], pr.to[o], mbase, nbase, pr.M, nlim, diag,
+                                         pr.sym != 0, tile, lane);
+                    } else {
+                        if (ph)
+                            chunk_store(v, ph, pr.ldo[o], pr.to[o], false, mbase, nbase, pr.M, nlim, diag,
+                                        pr.sym != 0, tile, lane);
+                        if (pl)
+                            chunk_store(v, pl, pr.ldo[o + 2], pr.to[o + 2], true, mbase, nbase, pr.M, nlim, diag,
+                                        pr.sym != 0, tile, lane);
+                    }
+                }
             }
             tc_fence_before();
             mbar_arrive(&bars->tmem_empty[acc]);
