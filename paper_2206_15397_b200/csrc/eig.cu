@@ -18,6 +18,8 @@
 #include <cfloat>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace rkfac_b200 {
@@ -143,6 +145,162 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(const EigDesc* __restrict
         }
         ed.evec[n - 1] = 0.0;
         if (n >= 1) ed.tau[n - 1] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------ tridiag on a CTA cluster
+// The same reduction spread over a cluster of 4 CTAs per factor (4 SMs; the 32 single-CTA factors left 116 SMs
+// idle).  CTA q owns the full rows i = q (mod 4) of the symmetric matrix (no packing, contiguous row dots), so:
+//   (B) p_i = tau A_i,: v is a local row dot (8 threads per row, shuffle tree), broadcast to the 4 CTAs through
+//       distributed shared memory together with per-warp partials of p^T v;
+//   (C) A_ij -= v_i w_j + w_i v_j on the owned rows (explicitly rounded products: row j's owner computes the
+//       mirror element bit-identically, the matrix stays exactly symmetric); the owners of the next column
+//       broadcast its entries and partial norms.
+// Two cluster barriers per column step; the reflector (beta, tau, v) is derived redundantly by every thread.
+constexpr int kTcC = 4;
+constexpr int kTcThreads = 256;
+constexpr int kTcWarps = kTcThreads / 32;
+constexpr int kTcG = 8;  // threads per row
+constexpr int kTcMaxN = 320;
+
+size_t tridiag_cluster_smem_bytes(int n) {
+    const int nloc = (n + kTcC - 1) / kTcC;
+    return ((size_t)nloc * n + 3 * (size_t)n + 3 * kTcC * kTcWarps) * sizeof(double);
+}
+
+__global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
+    tridiag_cluster_kernel(const EigDesc* __restrict__ descs) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int q = (int)cluster.block_rank();
+    const EigDesc& ed = descs[blockIdx.x / kTcC];
+    const int n = ed.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nloc = (n - q + kTcC - 1) / kTcC;  // rows i = q + 4 li, li < nloc
+    extern __shared__ __align__(16) double tsm[];
+    double* R = tsm;                                   // nloc x n
+    double* xb0 = R + (size_t)((n + kTcC - 1) / kTcC) * n;
+    double* const xbuf0 = xb0;                         // column below the diagonal (double-buffered)
+    double* const xbuf1 = xb0 + n;
+    double* pbuf = xb0 + 2 * n;                        // p (relative index)
+    double* sigp = pbuf + n;                           // [2][kTcC][kTcWarps]
+    double* pvp = sigp + 2 * kTcC * kTcWarps;          // [kTcC][kTcWarps]
+    // distributed-smem stores: element e of buffer buf in all 4 CTAs of the cluster
+    auto bcast = [&](double* buf, int e, double v) {
+#pragma unroll
+        for (int r = 0; r < kTcC; ++r) cluster.map_shared_rank(buf, r)[e] = v;
+    };
+    // owned rows, symmetrised from the FP32 core
+    for (int li = warp; li < nloc; li += kTcWarps) {
+        const int i = q + kTcC * li;
+        for (int j = lane; j < n; j += 32)
+            R[(size_t)li * n + j] =
+                0.5 * ((double)ed.A[(long long)i * ed.lda + j] + (double)ed.A[(long long)j * ed.lda + i]);
+    }
+    cluster.sync();  // every CTA of the cluster is running: distributed smem may be written
+    // first column: x_t = A[1 + t][0]
+    if (n >= 3) {
+        double s = 0.0;
+        for (int li = tid; li < nloc; li += kTcThreads) {
+            const int i = q + kTcC * li;
+            if (i >= 1) {
+                const double a = R[(size_t)li * n];
+                bcast(xbuf0, i - 1, a);
+                if (i >= 2) s += a * a;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) bcast(sigp, q * kTcWarps + warp, s);
+    }
+    cluster.sync();
+
+    const int g = tid / kTcG, sub = tid % kTcG;
+    constexpr int kGroups = kTcThreads / kTcG;
+    for (int k = 0; k + 2 < n; ++k) {
+        const int base = k + 1, m = n - base, cur = k & 1, nxt = cur ^ 1;
+        const double* x = cur ? xbuf1 : xbuf0;
+        double* xnext = cur ? xbuf0 : xbuf1;
+        // (A) reflector (fixed-order sums of the 32 partials)
+        double sig = sigp[cur * kTcC * kTcWarps + lane];
+        for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+        const double alpha = x[0];
+        double tau = 0.0, beta = alpha;
+        if (sig > 0.0) {
+            const double nrm = sqrt(alpha * alpha + sig);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+        }
+        const double scale = (sig > 0.0) ? 1.0 / (alpha - beta) : 0.0;
+        auto vof = [&](int t) { return t == 0 ? 1.0 : x[t] * scale; };
+        if (q == 0) {
+            if (tid == 0) {
+                ed.evec[k] = beta;
+                ed.tau[k] = tau;
+            }
+            for (int t = tid; t < m; t += kTcThreads) ed.refl[(long long)k * n + t] = vof(t);
+        }
+        if (q == (k & (kTcC - 1)) && tid == 0) ed.dvec[k] = R[(size_t)(k / kTcC) * n + k];
+        // (B) p_i = tau sum_j A_ij v_j over the owned rows i >= base
+        const int li0 = (base - q + kTcC - 1) / kTcC;  // first owned row >= base
+        double pvpart = 0.0;
+        for (int li = li0 + g; li < nloc; li += kGroups) {
+            const int i = q + kTcC * li;
+            const double* row = R + (size_t)li * n + base;
+            double acc = 0.0;
+            for (int t = sub; t < m; t += kTcG) acc += row[t] * vof(t);
+            const unsigned gmask = 0xFFu << (lane & ~(kTcG - 1));  // the row's 8 lanes (groups diverge in trip count)
+#pragma unroll
+            for (int o = kTcG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
+            const double p = tau * acc;
+            if (sub == 0) {
+                bcast(pbuf, i - base, p);
+                pvpart += p * vof(i - base);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) pvpart += __shfl_xor_sync(0xffffffffu, pvpart, o);
+        if (lane == 0) bcast(pvp, q * kTcWarps + warp, pvpart);
+        cluster.sync();
+        // (C) rank-2 update of the owned rows; the next column's entries and partial norms are broadcast
+        double pv = pvp[lane];
+        for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+        const double alpha2 = -0.5 * tau * pv;
+        double s2 = 0.0;
+        for (int li = li0 + g; li < nloc; li += kGroups) {
+            const int i = q + kTcC * li;
+            double* row = R + (size_t)li * n + base;
+            const double vr = vof(i - base), wr = pbuf[i - base] + alpha2 * vr;
+            for (int t = sub; t < m; t += kTcG) {
+                const double vc = vof(t), wc = pbuf[t] + alpha2 * vc;
+                const double a = __dsub_rn(row[t], __dadd_rn(__dmul_rn(vr, wc), __dmul_rn(wr, vc)));
+                row[t] = a;
+                if (t == 0 && i >= base + 1) {  // A[i][base]: next column entry i - base - 1
+                    bcast(xnext, i - base - 1, a);
+                    if (i >= base + 2) s2 += a * a;
+                }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0) bcast(sigp, (nxt * kTcC + q) * kTcWarps + warp, s2);
+        cluster.sync();
+    }
+    // trailing 2 x 2 (or 1 x 1)
+    if (tid == 0) {
+        if (n >= 2) {
+            if (q == ((n - 2) & (kTcC - 1))) ed.dvec[n - 2] = R[(size_t)((n - 2) / kTcC) * n + (n - 2)];
+            if (q == ((n - 1) & (kTcC - 1))) {
+                ed.dvec[n - 1] = R[(size_t)((n - 1) / kTcC) * n + (n - 1)];
+                ed.evec[n - 2] = R[(size_t)((n - 1) / kTcC) * n + (n - 2)];
+            }
+            if (q == 0) {
+                ed.tau[n - 2] = 0.0;
+                ed.evec[n - 1] = 0.0;
+                ed.tau[n - 1] = 0.0;
+            }
+        } else if (q == 0) {
+            ed.dvec[0] = R[0];
+            ed.evec[0] = 0.0;
+            ed.tau[0] = 0.0;
+        }
     }
 }
 
@@ -603,12 +761,19 @@ size_t tridiag_smem_bytes(int nmax) { return (size_t)nmax * (nmax + 1) / 2 * 8; 
 void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaStream_t s) {
     if (nfactors == 0) return;
     RKFAC_REQUIRE(nmax <= kMaxN, RKFAC_INVALID_ARGUMENT, "core size above 512 is not supported");
-    const size_t bytes = tridiag_smem_bytes(nmax);
-    const bool use_smem = bytes <= max_dynamic_smem((const void*)tridiag_kernel<true>);
-    auto k = use_smem ? tridiag_kernel<true> : tridiag_kernel<false>;
-    const size_t dyn = use_smem ? bytes : 0;
-    RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    k<<<nfactors, 1024, dyn, s>>>(d_descs);
+    const size_t cbytes = tridiag_cluster_smem_bytes(nmax);
+    if (nmax <= kTcMaxN && cbytes <= max_dynamic_smem((const void*)tridiag_cluster_kernel)) {
+        RKFAC_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)cbytes));
+        tridiag_cluster_kernel<<<nfactors * kTcC, kTcThreads, cbytes, s>>>(d_descs);
+    } else {
+        const size_t bytes = tridiag_smem_bytes(nmax);
+        const bool use_smem = bytes <= max_dynamic_smem((const void*)tridiag_kernel<true>);
+        auto k = use_smem ? tridiag_kernel<true> : tridiag_kernel<false>;
+        const size_t dyn = use_smem ? bytes : 0;
+        RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        k<<<nfactors, 1024, dyn, s>>>(d_descs);
+    }
     count_launch();
     RKFAC_CHECK_LAUNCH();
     const unsigned rchunks = (unsigned)std::max<int64_t>(1, ceil_div(std::max(rmax, 1), kBisE));
