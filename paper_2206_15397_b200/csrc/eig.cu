@@ -158,14 +158,32 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(const EigDesc* __restrict
 //       broadcast its entries and partial norms.
 // Two cluster barriers per column step; the reflector (beta, tau, v) is derived redundantly by every thread.
 constexpr int kTcC = 4;
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 512;
 constexpr int kTcWarps = kTcThreads / 32;
 constexpr int kTcG = 8;  // threads per row
 constexpr int kTcMaxN = 320;
 
+#ifdef RKFAC_TRC_TIMING  // per-phase clock64 stamps of one step (tools/eig_bench.cu)
+__device__ long long g_trc[16];
+#define TRC_PHASE(k, slot)                                                                     \
+    do {                                                                                       \
+        const long long t_ = clock64();                                                        \
+        if ((k) == RKFAC_TRC_TIMING && threadIdx.x == 0 && blockIdx.x == 0) g_trc[slot] = t_; \
+        __syncwarp();                                                                          \
+    } while (0)
+#else
+#define TRC_PHASE(k, slot)
+#endif
+
 size_t tridiag_cluster_smem_bytes(int n) {
     const int nloc = (n + kTcC - 1) / kTcC;
-    return ((size_t)nloc * n + 3 * (size_t)n + 3 * kTcC * kTcWarps) * sizeof(double);
+    return ((size_t)nloc * n + 5 * (size_t)n + 3 * kTcC * kTcWarps) * sizeof(double);
+}
+
+// Cluster barrier with release/acquire at cluster scope (the cooperative-groups sync adds a GPU-scope fence).
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
@@ -179,11 +197,12 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
     const int nloc = (n - q + kTcC - 1) / kTcC;  // rows i = q + 4 li, li < nloc
     extern __shared__ __align__(16) double tsm[];
     double* R = tsm;                                   // nloc x n
-    double* xb0 = R + (size_t)((n + kTcC - 1) / kTcC) * n;
-    double* const xbuf0 = xb0;                         // column below the diagonal (double-buffered)
-    double* const xbuf1 = xb0 + n;
-    double* pbuf = xb0 + 2 * n;                        // p (relative index)
-    double* sigp = pbuf + n;                           // [2][kTcC][kTcWarps]
+    double* const xbuf0 = R + (size_t)((n + kTcC - 1) / kTcC) * n;  // column below the diagonal (double-buffered)
+    double* const xbuf1 = xbuf0 + n;
+    double* pbuf = xbuf0 + 2 * n;                      // p (relative index)
+    double* vs = xbuf0 + 3 * n;                        // v of this step
+    double* ws = xbuf0 + 4 * n;                        // w of this step
+    double* sigp = xbuf0 + 5 * n;                      // [2][kTcC][kTcWarps]
     double* pvp = sigp + 2 * kTcC * kTcWarps;          // [kTcC][kTcWarps]
     // distributed-smem stores: element e of buffer buf in all 4 CTAs of the cluster
     auto bcast = [&](double* buf, int e, double v) {
@@ -212,16 +231,20 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) bcast(sigp, q * kTcWarps + warp, s);
     }
-    cluster.sync();
+    cluster_barrier();
 
     const int g = tid / kTcG, sub = tid % kTcG;
+    const unsigned gmask = 0xFFu << (lane & ~(kTcG - 1));  // the row's 8 lanes (groups diverge in trip count)
     constexpr int kGroups = kTcThreads / kTcG;
     for (int k = 0; k + 2 < n; ++k) {
         const int base = k + 1, m = n - base, cur = k & 1, nxt = cur ^ 1;
         const double* x = cur ? xbuf1 : xbuf0;
         double* xnext = cur ? xbuf0 : xbuf1;
-        // (A) reflector (fixed-order sums of the 32 partials)
-        double sig = sigp[cur * kTcC * kTcWarps + lane];
+        TRC_PHASE(k, 0);
+        // (A) reflector (fixed-order sums of the 32 partials), v into smem
+        double sig = 0.0;
+#pragma unroll
+        for (int e = lane; e < kTcC * kTcWarps; e += 32) sig += sigp[cur * kTcC * kTcWarps + e];
         for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
         const double alpha = x[0];
         double tau = 0.0, beta = alpha;
@@ -231,57 +254,84 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
             tau = (beta - alpha) / beta;
         }
         const double scale = (sig > 0.0) ? 1.0 / (alpha - beta) : 0.0;
-        auto vof = [&](int t) { return t == 0 ? 1.0 : x[t] * scale; };
-        if (q == 0) {
-            if (tid == 0) {
-                ed.evec[k] = beta;
-                ed.tau[k] = tau;
-            }
-            for (int t = tid; t < m; t += kTcThreads) ed.refl[(long long)k * n + t] = vof(t);
+        for (int t = tid; t < m; t += kTcThreads) {
+            const double v = t == 0 ? 1.0 : x[t] * scale;
+            vs[t] = v;
+            if (q == 0) ed.refl[(long long)k * n + t] = v;
+        }
+        if (q == 0 && tid == 0) {
+            ed.evec[k] = beta;
+            ed.tau[k] = tau;
         }
         if (q == (k & (kTcC - 1)) && tid == 0) ed.dvec[k] = R[(size_t)(k / kTcC) * n + k];
+        __syncthreads();
+        TRC_PHASE(k, 1);
         // (B) p_i = tau sum_j A_ij v_j over the owned rows i >= base
         const int li0 = (base - q + kTcC - 1) / kTcC;  // first owned row >= base
         double pvpart = 0.0;
         for (int li = li0 + g; li < nloc; li += kGroups) {
             const int i = q + kTcC * li;
             const double* row = R + (size_t)li * n + base;
-            double acc = 0.0;
-            for (int t = sub; t < m; t += kTcG) acc += row[t] * vof(t);
-            const unsigned gmask = 0xFFu << (lane & ~(kTcG - 1));  // the row's 8 lanes (groups diverge in trip count)
+            double a0 = 0.0, a1 = 0.0;
+            int t = sub;
+            for (; t + kTcG < m; t += 2 * kTcG) {
+                a0 += row[t] * vs[t];
+                a1 += row[t + kTcG] * vs[t + kTcG];
+            }
+            if (t < m) a0 += row[t] * vs[t];
+            double acc = a0 + a1;
 #pragma unroll
             for (int o = kTcG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
             const double p = tau * acc;
             if (sub == 0) {
                 bcast(pbuf, i - base, p);
-                pvpart += p * vof(i - base);
+                pvpart += p * vs[i - base];
             }
         }
         for (int o = 16; o > 0; o >>= 1) pvpart += __shfl_xor_sync(0xffffffffu, pvpart, o);
         if (lane == 0) bcast(pvp, q * kTcWarps + warp, pvpart);
-        cluster.sync();
+        TRC_PHASE(k, 2);
+        cluster_barrier();
+        TRC_PHASE(k, 3);
         // (C) rank-2 update of the owned rows; the next column's entries and partial norms are broadcast
-        double pv = pvp[lane];
+        double pv = 0.0;
+#pragma unroll
+        for (int e = lane; e < kTcC * kTcWarps; e += 32) pv += pvp[e];
         for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
         const double alpha2 = -0.5 * tau * pv;
+        for (int t = tid; t < m; t += kTcThreads) ws[t] = pbuf[t] + alpha2 * vs[t];
+        __syncthreads();
         double s2 = 0.0;
         for (int li = li0 + g; li < nloc; li += kGroups) {
             const int i = q + kTcC * li;
             double* row = R + (size_t)li * n + base;
-            const double vr = vof(i - base), wr = pbuf[i - base] + alpha2 * vr;
-            for (int t = sub; t < m; t += kTcG) {
-                const double vc = vof(t), wc = pbuf[t] + alpha2 * vc;
-                const double a = __dsub_rn(row[t], __dadd_rn(__dmul_rn(vr, wc), __dmul_rn(wr, vc)));
+            const double vr = vs[i - base], wr = ws[i - base];
+            // explicitly rounded products: row j's owner computes the mirror element bit-identically
+            auto upd = [&](int t) {
+                const double a = __dsub_rn(row[t], __dadd_rn(__dmul_rn(vr, ws[t]), __dmul_rn(wr, vs[t])));
                 row[t] = a;
-                if (t == 0 && i >= base + 1) {  // A[i][base]: next column entry i - base - 1
+                return a;
+            };
+            int t = sub;
+            if (sub == 0) {  // column base: the next x
+                const double a = upd(0);
+                if (i >= base + 1) {
                     bcast(xnext, i - base - 1, a);
                     if (i >= base + 2) s2 += a * a;
                 }
+                t = kTcG;
             }
+            for (; t + kTcG < m; t += 2 * kTcG) {
+                upd(t);
+                upd(t + kTcG);
+            }
+            if (t < m) upd(t);
         }
         for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
         if (lane == 0) bcast(sigp, (nxt * kTcC + q) * kTcWarps + warp, s2);
-        cluster.sync();
+        TRC_PHASE(k, 4);
+        cluster_barrier();
+        TRC_PHASE(k, 5);
     }
     // trailing 2 x 2 (or 1 x 1)
     if (tid == 0) {
@@ -302,6 +352,7 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
             ed.tau[0] = 0.0;
         }
     }
+    cluster.sync();  // no CTA leaves while others may still write into its shared memory
 }
 
 // ------------------------------------------------------------------------------------- tridiagonal eig
