@@ -805,6 +805,177 @@ __global__ void __launch_bounds__(256) backxform_kernel(const EigDesc* __restric
     }
 }
 
+// Blocked back transformation with the compact WY form (LAPACK dlarft/dlarfb, forward columnwise): the 32
+// reflectors k0..k0+31 act as I - V T V^T, applied to the CTA's 32 eigenvector columns from the last block to
+// the first, so 8 blocks of three small products (W = V^T Z, W = T W, Z -= V W) replace 228 dependent reflector
+// steps.  T is formed in the CTA from G = V^T V (upper triangle): T_ii = tau_i, T(0:i, i) = -tau_i T G(0:i, i).
+#ifdef RKFAC_TRC_TIMING
+__device__ long long g_bx[8][8];
+#define BX_PHASE(b, slot)                                                                       \
+    do {                                                                                        \
+        const long long t_ = clock64();                                                         \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && (b) < 8) g_bx[b][slot] = t_; \
+        __syncwarp();                                                                           \
+    } while (0)
+#else
+#define BX_PHASE(b, slot)
+#endif
+constexpr int kWyB = 32;          // reflectors per block
+constexpr int kWyC = 64;          // eigenvector columns per CTA (2 per lane)
+constexpr int kWyThreads = 512;
+constexpr int kWyWarps = kWyThreads / 32;
+constexpr int kWyMaxN = 256;
+constexpr int kWyP = kWyB + 2;    // padded pitch of V and G (doubles; even: 16-byte pairs)
+constexpr int kWyWP = kWyC + 1;   // padded pitch of W
+
+size_t backxform_wy_smem_bytes(int n) {
+    return ((size_t)n * kWyC + (size_t)n * kWyP + 2 * kWyB * kWyP + kWyB * kWyWP + kWyB) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(kWyThreads) backxform_wy_kernel(const EigDesc* __restrict__ descs) {
+    const EigDesc& ed = descs[blockIdx.y];
+    const int n = ed.n, r = ed.r;
+    const int c0 = blockIdx.x * kWyC;
+    if (c0 >= r) return;
+    const int nc = min(kWyC, r - c0);
+    extern __shared__ __align__(16) double wsm[];
+    double* Zs = wsm;                          // [n][64]
+    double* V = Zs + (size_t)n * kWyC;         // [M][kWyP]
+    double* G = V + (size_t)n * kWyP;          // [32][kWyP]
+    double* T = G + kWyB * kWyP;               // [32][kWyP]
+    double* W = T + kWyB * kWyP;               // [32][kWyWP]
+    double* taus = W + kWyB * kWyWP;           // [32]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < n * kWyC; e += kWyThreads) {
+        const int i = e / kWyC, c = e % kWyC;
+        Zs[e] = (c < nc) ? ed.z[(long long)i * r + c0 + c] : 0.0;
+    }
+    const int nref = n - 2;  // reflectors 0 .. n-3
+    const int nblk = nref > 0 ? (nref + kWyB - 1) / kWyB : 0;
+    for (int b = nblk - 1; b >= 0; --b) {
+        const int k0 = b * kWyB, nb = min(kWyB, nref - k0);
+        const int r0 = k0 + 1, M = n - r0;  // rows r0 .. n-1
+        __syncthreads();
+        BX_PHASE(b, 0);
+        // V[rel][j] = v_{k0+j}[rel - j] (rel >= j), unit at rel == j, zero above; 4 independent loads per thread
+        for (int e0 = tid; e0 < M * kWyB; e0 += 4 * kWyThreads) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * kWyThreads, rel = e / kWyB, j = e % kWyB;
+                v[u] = (e < M * kWyB && j < nb && rel >= j) ? ed.refl[(long long)(k0 + j) * n + (rel - j)] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * kWyThreads;
+                if (e < M * kWyB) V[(e / kWyB) * kWyP + e % kWyB] = v[u];
+            }
+        }
+        if (tid < kWyB) taus[tid] = (tid < nb) ? ed.tau[k0 + tid] : 0.0;
+        __syncthreads();
+        BX_PHASE(b, 1);
+        // G = V^T V (upper triangle) and W = V^T Z: warp -> rows jj, jj+1 of G/W (a 16-byte broadcast pair of V),
+        // lane -> column i of G and columns lane, lane + 32 of W; six independent chains per thread
+        {
+            const int jj = 2 * warp;  // kWyWarps * 2 == kWyB
+            const int i = lane;
+            double g0 = 0.0, g1 = 0.0, w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+            for (int rel = jj; rel < M; ++rel) {
+                const double2 vp = *reinterpret_cast<const double2*>(&V[rel * kWyP + jj]);
+                const double vi = V[rel * kWyP + i];
+                const double z0 = Zs[(r0 + rel) * kWyC + lane], z1 = Zs[(r0 + rel) * kWyC + lane + 32];
+                g0 += vp.x * vi;
+                g1 += vp.y * vi;
+                w00 += vp.x * z0;
+                w01 += vp.x * z1;
+                w10 += vp.y * z0;
+                w11 += vp.y * z1;
+            }
+            G[jj * kWyP + i] = (jj < i) ? g0 : 0.0;
+            G[(jj + 1) * kWyP + i] = (jj + 1 < i) ? g1 : 0.0;
+            W[jj * kWyWP + lane] = w00;
+            W[jj * kWyWP + lane + 32] = w01;
+            W[(jj + 1) * kWyWP + lane] = w10;
+            W[(jj + 1) * kWyWP + lane + 32] = w11;
+        }
+        __syncthreads();
+        BX_PHASE(b, 2);
+        // T = (diag(1/tau) + striu(V^T V))^{-1} (compact WY, forward columnwise): lane j back-substitutes column j,
+        // T(i, j) = -tau_i sum_{l=i+1}^{j} G(i, l) T(l, j), T(j, j) = tau_j (tau_i = 0 gives a zero row and column)
+        if (warp == 0) {
+            double t[kWyB];
+            const int j = lane;
+#pragma unroll
+            for (int i = kWyB - 1; i >= 0; --i) {
+                double acc = 0.0;
+#pragma unroll
+                for (int l = i + 1; l < kWyB; ++l) acc += G[i * kWyP + l] * t[l];  // t[l] = 0 for l > j
+                t[i] = (i > j) ? 0.0 : (i == j ? taus[j] : -taus[i] * acc);
+            }
+#pragma unroll
+            for (int i = 0; i < kWyB; ++i) T[i * kWyP + j] = t[i];
+        }
+        __syncthreads();
+        BX_PHASE(b, 3);
+        // W <- T W (T upper triangular; the stored zeros are summed), in registers then back
+        double tw[2][kWyB / kWyWarps];
+#pragma unroll
+        for (int u = 0; u < kWyB / kWyWarps; ++u) {
+            const int j = warp + u * kWyWarps;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < kWyB; ++l) {
+                const double t = T[j * kWyP + l];
+                a0 += t * W[l * kWyWP + lane];
+                a1 += t * W[l * kWyWP + lane + 32];
+            }
+            tw[0][u] = a0;
+            tw[1][u] = a1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kWyB / kWyWarps; ++u) {
+            W[(warp + u * kWyWarps) * kWyWP + lane] = tw[0][u];
+            W[(warp + u * kWyWarps) * kWyWP + lane + 32] = tw[1][u];
+        }
+        __syncthreads();
+        BX_PHASE(b, 4);
+        // Z -= V W: a warp takes 4 rows at a time (the W loads are shared), lanes over 2 columns
+        for (int rel0 = 4 * warp; rel0 < M; rel0 += 4 * kWyWarps) {
+            double acc[4][2] = {};
+#pragma unroll 4
+            for (int j = 0; j < kWyB; j += 2) {
+                const double wa0 = W[j * kWyWP + lane], wb0 = W[j * kWyWP + lane + 32];
+                const double wa1 = W[(j + 1) * kWyWP + lane], wb1 = W[(j + 1) * kWyWP + lane + 32];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rel = min(rel0 + u, M - 1);
+                    const double2 vp = *reinterpret_cast<const double2*>(&V[rel * kWyP + j]);
+                    acc[u][0] += vp.x * wa0 + vp.y * wa1;
+                    acc[u][1] += vp.x * wb0 + vp.y * wb1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (rel0 + u < M) {
+                    Zs[(r0 + rel0 + u) * kWyC + lane] -= acc[u][0];
+                    Zs[(r0 + rel0 + u) * kWyC + lane + 32] -= acc[u][1];
+                }
+        }
+        __syncthreads();
+        BX_PHASE(b, 5);
+    }
+    __syncthreads();
+    for (long long e = tid; e < (long long)n * kWyC; e += kWyThreads) {
+        const int i = (int)(e / kWyC), c = (int)(e % kWyC);
+        if (c < nc) {
+            const float v = (float)Zs[e];
+            ed.Pt[(long long)(c0 + c) * ed.ldpt + i] = v;
+            ed.Ptlo[(long long)(c0 + c) * ed.ldpt + i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        }
+    }
+}
+
 }  // namespace
 
 size_t tridiag_smem_bytes(int nmax) { return (size_t)nmax * (nmax + 1) / 2 * 8; }
@@ -840,10 +1011,17 @@ void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaSt
     reorth_kernel<<<nfactors, 32, 0, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
-    const size_t bx = (size_t)nmax * kBxCols * 8;
-    RKFAC_CUDA(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bx));
     dim3 grid((unsigned)ceil_div(std::max(rmax, 1), kBxCols), (unsigned)nfactors);
-    backxform_kernel<<<grid, 256, bx, s>>>(d_descs);
+    const size_t wyb = backxform_wy_smem_bytes(nmax);
+    if (nmax <= kWyMaxN && wyb <= max_dynamic_smem((const void*)backxform_wy_kernel)) {
+        RKFAC_CUDA(cudaFuncSetAttribute(backxform_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wyb));
+        dim3 gwy((unsigned)ceil_div(std::max(rmax, 1), kWyC), (unsigned)nfactors);
+        backxform_wy_kernel<<<gwy, kWyThreads, wyb, s>>>(d_descs);
+    } else {
+        const size_t bx = (size_t)nmax * kBxCols * 8;
+        RKFAC_CUDA(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bx));
+        backxform_kernel<<<grid, 256, bx, s>>>(d_descs);
+    }
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

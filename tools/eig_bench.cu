@@ -62,6 +62,11 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(t, g_trc, sizeof(t));
     printf("step %d: reflector %lld, B %lld, sync1 %lld, C %lld, sync2 %lld cycles\n", RKFAC_TRC_TIMING, t[1] - t[0],
            t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+    long long bx[8][8];
+    cudaMemcpyFromSymbol(bx, g_bx, sizeof(bx));
+    for (int b = 7; b >= 0; --b)
+        printf("wy block %d: V %lld, G/W %lld, T %lld, TW %lld, Z %lld\n", b, bx[b][1] - bx[b][0], bx[b][2] - bx[b][1],
+               bx[b][3] - bx[b][2], bx[b][4] - bx[b][3], bx[b][5] - bx[b][4]);
 #endif
     std::vector<double> dv(n);
     cudaMemcpy(dv.data(), h[0].evals, sizeof(double) * 5, cudaMemcpyDeviceToHost);
