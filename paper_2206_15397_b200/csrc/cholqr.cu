@@ -48,11 +48,13 @@ __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__
 
 __host__ __device__ __forceinline__ int rup4(int x) { return (x + 3) & ~3; }
 
-// Offset of row i in the padded packed layout: sum_{t<i} rup4(t+1).
+// Offset of row i in the padded packed layout: sum_{t<i} rup4(t+1) plus 4 skew elements after every block of 4
+// rows.  rup4(t+1) for t = 4a+b is 4a+4, so block a starts at 8a(a+1); without the skew the rows 4a (the first rows
+// of the 4x4 register tiles that consecutive threads take) all start in the same two 16-byte bank groups (16-way
+// conflicts on LDS.128); with it, 8 consecutive blocks start in 8 distinct groups.
 __host__ __device__ __forceinline__ int prow(int i) {
-    // rup4(t+1) for t = 4a+b (b=0..3) is 4a+4 => a block of 4 rows [4a, 4a+4) occupies 16a+16
     const int a = i >> 2, b = i & 3;
-    return 8 * a * (a + 1) + b * (4 * a + 4);
+    return 8 * a * (a + 1) + b * (4 * a + 4) + 4 * a;
 }
 
 // bytes of the small per-factor state carved at the start of the dynamic smem (16-byte multiple)
@@ -63,6 +65,14 @@ __host__ __device__ __forceinline__ int cholinv_state_bytes(int n, int es) {
 template <class T> struct Vec4T;
 template <> struct Vec4T<float> { using type = float4; };
 template <> struct Vec4T<double> { using type = double4; };
+
+template <class T>
+__device__ __forceinline__ void st4(T* p, T a, T b, T c, T d) {
+    using V = typename Vec4T<T>::type;
+    V x;
+    x.x = a; x.y = b; x.z = c; x.w = d;
+    *reinterpret_cast<V*>(p) = x;
+}
 
 template <class T>
 __device__ __forceinline__ void ld4(const T* p, T (&v)[4]) {
@@ -80,17 +90,22 @@ __device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
 template <>
 __device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
 
-// Lower-triangular tile enumeration of a trapezoid: column tiles [0, CJ), row tiles [J, TR) (column-major):
-// t -> (I, J) with offset(J) = J*TR - J(J-1)/2.
-__device__ __forceinline__ void trap_tile(int t, int TR, int& I, int& J) {
-    // solve J*TR - J(J-1)/2 <= t for the largest J
-    const float b = (float)TR + 0.5f;
-    int j = (int)(b - sqrtf(fmaxf(b * b - 2.f * (float)t, 0.f)));
-    j = max(j, 0);
-    while (j > 0 && j * TR - j * (j - 1) / 2 > t) --j;
-    while ((j + 1) * TR - (j + 1) * j / 2 <= t) ++j;
-    J = j;
-    I = j + (t - (j * TR - j * (j - 1) / 2));
+// Lower-triangular tile enumeration of a trapezoid, row-major: row tiles I in [0, TR), column tiles J in
+// [0, min(I + 1, CJ)).  Consecutive threads take consecutive J of the same row tile, so the A operand rows are
+// broadcast and the read-modify-write of the output is contiguous within a warp.
+__device__ __forceinline__ void trap_tile(int t, int CJ, int& I, int& J) {
+    const int tri = CJ * (CJ + 1) / 2;
+    if (t < tri) {
+        int i = (int)((sqrtf(8.f * (float)t + 1.f) - 1.f) * 0.5f);
+        while (i * (i + 1) / 2 > t) --i;
+        while ((i + 1) * (i + 2) / 2 <= t) ++i;
+        I = i;
+        J = t - i * (i + 1) / 2;
+    } else {
+        const int u = t - tri;
+        I = CJ + u / CJ;
+        J = u - (I - CJ) * CJ;
+    }
 }
 
 template <class TG, class T, bool kSmem>
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
         const int ntiles = CJ * TR - CJ * (CJ - 1) / 2;
         for (int t = tid - t0; t < ntiles; t += nt) {
             int I, J;
-            trap_tile(t, TR, I, J);
+            trap_tile(t, CJ, I, J);
             const T* ra[4];
             const T* rb[4];
 #pragma unroll
@@ -250,30 +265,51 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
                 rb[u] = L + prow(min(c0 + J * 4 + u, n - 1)) + J0;
             }
             T acc[4][4] = {};
+            if (nb == kNB) {  // full panel: branch-free K loop, all loads can be hoisted by the scheduler
 #pragma unroll
-            for (int c4 = 0; c4 < kNB; c4 += 4) {
-                if (c4 < nb) {
+                for (int c4 = 0; c4 < kNB; c4 += 4) {
                     T av[4][4], bv[4][4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) { ld4(ra[u] + c4, av[u]); ld4(rb[u] + c4, bv[u]); }
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
-                        if (c4 + c < nb)
 #pragma unroll
-                            for (int u = 0; u < 4; ++u)
+                        for (int u = 0; u < 4; ++u)
 #pragma unroll
-                                for (int v = 0; v < 4; ++v) acc[u][v] += av[u][c] * bv[v][c];
+                            for (int v = 0; v < 4; ++v) acc[u][v] += av[u][c] * bv[v][c];
+                }
+            } else {
+#pragma unroll
+                for (int c4 = 0; c4 < kNB; c4 += 4) {
+                    if (c4 < nb) {
+                        T av[4][4], bv[4][4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) { ld4(ra[u] + c4, av[u]); ld4(rb[u] + c4, bv[u]); }
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (c4 + c < nb)
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) acc[u][v] += av[u][c] * bv[v][c];
+                    }
                 }
             }
+            const int j0 = c0 + J * 4;
+            const bool full = I > J && j0 + 3 < c1;  // strictly below the diagonal, whole column group in range
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int ii = c0 + I * 4 + u;
                 if (ii >= n) continue;
-                T* wr = L + prow(ii);
+                T* wr = L + prow(ii) + j0;
+                if (full) {
+                    T w4[4];
+                    ld4(wr, w4);
+                    st4(wr, w4[0] - acc[u][0], w4[1] - acc[u][1], w4[2] - acc[u][2], w4[3] - acc[u][3]);
+                } else {
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int jj = c0 + J * 4 + v;
-                    if (jj <= ii && jj < c1) wr[jj] -= acc[u][v];
+                    for (int v = 0; v < 4; ++v)
+                        if (j0 + v <= ii && j0 + v < c1) wr[v] -= acc[u][v];
                 }
             }
         }
@@ -447,11 +483,7 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
                 if (have) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (r0 + u < n) {
-                            T* wr = L + prow(r0 + u) + c0;
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) wr[v] = acc[u][v];
-                        }
+                        if (r0 + u < n) st4(L + prow(r0 + u) + c0, acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
                 }
                 __syncthreads();
             }

@@ -95,7 +95,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         o.L32 = c.take<float>(w * wp);
         o.L32lo = c.take<float>(w * wp);
         o.flags = c.take<int>(w + 1);
-        o.chol = c.take<double>(w * (w + 1) / 2 + 4 * w);  // padded packed triangle (cholqr.cu prow)
+        o.chol = c.take<double>(w * (w + 1) / 2 + 8 * w + 16);  // padded, skewed packed triangle (cholqr.cu prow)
         o.core = c.take<float>(w * w);
         o.esc = c.take<double>(w * (w + 1) / 2);
         o.refl = c.take<double>(w * w);

@@ -19,7 +19,7 @@ uint64_t& launch_counter() {
 
 using namespace rkfac_b200;
 
-__global__ void make_gram(float* G, double* G64, int w, int d, int nf) {
+__global__ void make_gram(float* G, double* G64, int w, int wp, int d, int nf) {
     // G = Y^T Y / d + 1e-3 I for a deterministic pseudo-random Y (w x d), one CTA row per (factor, i)
     const int f = blockIdx.y, i = blockIdx.x;
     for (int j = threadIdx.x; j < w; j += blockDim.x) {
@@ -32,8 +32,8 @@ __global__ void make_gram(float* G, double* G64, int w, int d, int nf) {
             s += a * b;
         }
         s = s / d + (i == j ? 1e-3 : 0.0);
-        G[((size_t)f * w + i) * w + j] = (float)s;
-        G64[((size_t)f * w + i) * w + j] = s;
+        G[((size_t)f * w + i) * wp + j] = (float)s;
+        G64[((size_t)f * w + i) * wp + j] = s;
     }
 }
 
@@ -46,20 +46,20 @@ int main(int argc, char** argv) {
     double *G64, *L64;
     int* flags;
     void* scratch;
-    cudaMalloc(&G, sizeof(float) * nf * w * w);
-    cudaMalloc(&G64, sizeof(double) * nf * w * w);
+    cudaMalloc(&G, sizeof(float) * nf * w * wp);
+    cudaMalloc(&G64, sizeof(double) * nf * w * wp);
     cudaMalloc(&Li, sizeof(float) * nf * w * wp);
     cudaMalloc(&Llo, sizeof(float) * nf * w * wp);
     cudaMalloc(&L64, sizeof(double) * nf * w * wp);
     cudaMalloc(&flags, sizeof(int) * nf * (w + 1));
     cudaMalloc(&scratch, sizeof(double) * nf * (size_t)prow(w + 4));
-    make_gram<<<dim3(w, nf), 128>>>(G, G64, w, 256, nf);
+    make_gram<<<dim3(w, nf), 128>>>(G, G64, w, wp, 256, nf);
     std::vector<CholDesc> h(nf);
     for (int f = 0; f < nf; ++f) {
         CholDesc& c = h[f];
         c.w = w;
-        c.G = fp64 ? (const void*)(G64 + (size_t)f * w * w) : (const void*)(G + (size_t)f * w * w);
-        c.ldg = w;
+        c.G = fp64 ? (const void*)(G64 + (size_t)f * w * wp) : (const void*)(G + (size_t)f * w * wp);
+        c.ldg = wp;
         c.Linv = fp64 ? (void*)(L64 + (size_t)f * w * wp) : (void*)(Li + (size_t)f * w * wp);
         c.ldl = wp;
         c.Linv_lo = fp64 ? nullptr : (void*)(Llo + (size_t)f * w * wp);
@@ -102,7 +102,10 @@ int main(int argc, char** argv) {
     // verify: max |Linv G Linv^T - I| on factor 0 (FP32 only)
     if (!fp64) {
         std::vector<float> hg((size_t)w * w), hl((size_t)w * wp);
-        cudaMemcpy(hg.data(), G, sizeof(float) * w * w, cudaMemcpyDeviceToHost);
+        std::vector<float> hgp((size_t)w * wp);
+        cudaMemcpy(hgp.data(), G, sizeof(float) * w * wp, cudaMemcpyDeviceToHost);
+        for (int i = 0; i < w; ++i)
+            for (int j = 0; j < w; ++j) hg[(size_t)i * w + j] = hgp[(size_t)i * wp + j];
         cudaMemcpy(hl.data(), Li, sizeof(float) * w * wp, cudaMemcpyDeviceToHost);
         std::vector<double> t((size_t)w * w, 0.0);
         for (int i = 0; i < w; ++i)
