@@ -615,6 +615,29 @@ __global__ void __launch_bounds__(1024) complete_kernel(const CompleteDesc* __re
     }
 }
 
+// Rank-deficient columns of the final basis: the flagged (zero) rows of Qt get deterministic pseudo-random
+// candidates, which the CholeskyQR2 pass that follows orthonormalises together with the good columns (span of the
+// good columns unchanged).  Intermediate bases simply keep their zero columns: X maps them to zero, so they stay
+// flagged and never perturb the power iteration (rank(X) < w means the good columns already span range(X)).
+__global__ void __launch_bounds__(256) fill_kernel(const CompleteDesc* __restrict__ descs) {
+    const CompleteDesc& cd = descs[blockIdx.y];
+    if (*cd.nflags == 0) return;
+    const int w = cd.w, d = cd.d;
+    const float unit = sqrtf(12.f / (float)d);  // candidates of about unit norm: the CholeskyQR that follows sees a
+                                                // well-conditioned Gram (good columns are unit norm too)
+    for (int k = 0; k < w; ++k) {
+        if (!cd.flags[k]) continue;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+            const float v = unit * cand_value(k, 0, i);
+            const float l = v - tf32_trunc(v);
+            cd.Qt[(long long)k * cd.ldq + i] = v;
+            if (cd.Qt_lo) cd.Qt_lo[(long long)k * cd.ldq + i] = l;
+            if (cd.Q) cd.Q[(long long)i * cd.ldr + k] = v;
+            if (cd.Q_lo) cd.Q_lo[(long long)i * cd.ldr + k] = l;
+        }
+    }
+}
+
 }  // namespace
 
 size_t cholinv_smem_bytes(int wmax, bool fp64) {
@@ -636,6 +659,13 @@ void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, 
     const size_t dyn = use_smem ? bytes : (size_t)cholinv_state_bytes(wmax, fp64 ? 8 : 4);
     RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     k<<<nfactors, kCholThreads, dyn, s>>>(d_descs, tol);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+}
+
+void launch_fill(const CompleteDesc* d_descs, int nfactors, cudaStream_t s) {
+    if (nfactors == 0) return;
+    fill_kernel<<<dim3(8, nfactors), 256, 0, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

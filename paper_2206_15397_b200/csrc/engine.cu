@@ -487,7 +487,7 @@ void Plan::orth(int src, bool fp64, cudaStream_t s) {
         launch_cholinv(d_chol32_.as<CholDesc>(), n, wmax_, false, false, kTol32, s);
         tri_[src]->launch(s);
     }
-    launch_complete(d_complete_[src].as<CompleteDesc>(), n, s);
+    // rank-deficient columns stay zero here; the final basis is completed in decompose()
 }
 
 // ---- stage timing: CUDA events from a pool, recorded on the context stream, harvested after the caller syncs
@@ -565,9 +565,13 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     }
     if (!last_fp64) {  // CholeskyQR2: second pass so the final basis is orthonormal to FP32 rounding
         mark(kOrth, true);
+        launch_fill(d_complete_[cur_q ^ 1].as<CompleteDesc>(), n, s);  // candidates for flagged columns
         orth(cur_q, false, s);
+        launch_complete(d_complete_[cur_q].as<CompleteDesc>(), n, s);  // last resort (normally nothing flagged)
         mark(kOrth, false);
         cur_q ^= 1;
+    } else {
+        launch_complete(d_complete_[cur_q ^ 1].as<CompleteDesc>(), n, s);
     }
     const int y = cur_q ^ 1;
     timed_xq(y);

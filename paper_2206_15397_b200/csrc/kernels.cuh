@@ -48,6 +48,8 @@ struct CompleteDesc {
     long long ldr;
 };
 void launch_complete(const CompleteDesc* d_descs, int nfactors, cudaStream_t s);
+// Pseudo-random candidates into the flagged rows of a basis (before the final CholeskyQR2 pass).
+void launch_fill(const CompleteDesc* d_descs, int nfactors, cudaStream_t s);
 
 struct EigDesc {
     int n, r;            // core size (w) and number of eigenpairs wanted

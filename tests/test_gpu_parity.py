@@ -313,3 +313,55 @@ def test_batched_step_matches_per_layer_oracle(port, cuda):
             decs.append((u0, d0))
         s0 = port.precondition(decs[0][0], decs[0][1], decs[1][0], decs[1][1], lam, grads[l])
         assert rel_fro(np64(step.outs[l]), s0) < TOL
+
+
+@pytest.mark.parametrize("d,e,steps", [(1153, 0.0, 6), (1153, 1.0, 20)])
+def test_batched_step_large_factor_vgg_sketch(port, cuda, d, e, steps):
+    """VGG16 sketch sizes (r=220, p=10, q=4) on a factor large enough for split-K Gram products, for an isotropic
+    (e=0: well conditioned, slowly decaying) and a decaying (e=1) spectrum."""
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    r, p, q, n = 220, 10, 4, 128
+    step = rk.BatchedStep([rk.LayerSpec(d, 64)], rank=r, oversampling=p, power_iters=q,
+                          method=rk.DecompMethod.SREVD, n_samples=[n], device=0)
+    x = build_factor(port, d, n, steps, e, f=0)
+    step.factors[0].copy_(t32(x, cuda))
+    step.factors[1].copy_(t32(build_factor(port, 64, n, steps, e, f=1), cuda))
+    step.decompose(OMEGA_ROOT, 0)
+    torch.cuda.synchronize()
+    u0, d0, _ = port.srevd(x, r, p, q, port.substream(OMEGA_ROOT, 0, 0), 0)
+    lr = step.lowrank(0)
+    assert recon_err(np64(lr.u), np64(lr.d), u0, d0) < TOL
+    assert eig_err(np64(lr.d), d0) < TOL
+    assert orth_err(np64(lr.u)) < 1e-5
+
+
+def test_rank_deficient_ea_start_is_fast_and_exact(port, cuda):
+    """First K-FAC step from zero-init EA: rank(X) = n = 128 < w = 230, so ~100 sketch columns are
+    rank deficient in every orthonormalisation.  The decomposition must stay exact on range(X) (recovery of X to
+    FP32 accuracy) and must not fall off a performance cliff (the completion runs once, on the final basis)."""
+    import time
+
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    d, n, r, p, q = 1153, 128, 220, 10, 4
+    step = rk.BatchedStep([rk.LayerSpec(d, 64)], rank=r, oversampling=p, power_iters=q,
+                          method=rk.DecompMethod.SREVD, n_samples=[n], device=0)
+    x = build_factor(port, d, n, 1, 1.0, f=0)  # one EA update from zero: rank 128
+    step.factors[0].copy_(t32(x, cuda))
+    step.factors[1].copy_(t32(build_factor(port, 64, n, 1, 1.0, f=1), cuda))
+    step.decompose(OMEGA_ROOT, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    step.decompose(OMEGA_ROOT, 0)
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    lr = step.lowrank(0)
+    u, dv = np64(lr.u), np64(lr.d)
+    assert np.linalg.norm(x - (u * dv) @ u.T) <= 1e-5 * np.linalg.norm(x)
+    # the ~100 null-space columns are eigenvectors of FP32-noise-level eigenvalues of the core: orthonormal to a few
+    # FP32 ulps times sqrt(w) rather than to one
+    assert orth_err(u) < 5e-5
+    assert elapsed < 0.1, elapsed
