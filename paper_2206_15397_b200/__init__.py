@@ -480,3 +480,93 @@ class BatchedStep:
             self.ctx.lib.rkfac_plan_destroy(self.h)
         except Exception:
             pass
+
+
+class StreamedStep:
+    """The batched step split into ``groups`` independent layer groups, each a :class:`BatchedStep` (its own plan)
+    run on its own CUDA stream and joined back into the caller's stream.
+
+    The per-factor kernels of the decomposition are latency-bound on a few SMs (Cholesky-inverse: one CTA per factor,
+    the tridiagonalisation: one 4-CTA cluster per factor); running a second group's tensor-core stages meanwhile
+    fills the idle SMs.  Groups are formed by LPT on the decomposition cost, exactly like the multi-GPU shards, and
+    factor tags stay global, so every result is bitwise identical to the single-plan step.  Public surface (factors,
+    samples, grads, outs, lowrank, stages) mirrors BatchedStep in the original layer order.
+    """
+
+    def __init__(self, layers: Sequence[LayerSpec], groups: int = 2, rank: int = 220, oversampling: int = 10,
+                 power_iters: int = 4, method: DecompMethod = DecompMethod.SREVD, n_samples: Sequence[int] = (),
+                 device: int = 0, factor_indices: Optional[Sequence[int]] = None):
+        from .partition import layer_cost, lpt_partition
+
+        torch = _torch()
+        self.layers = list(layers)
+        self.device = device
+        self.method = method
+        nl = len(self.layers)
+        tags = list(factor_indices) if factor_indices is not None else list(range(2 * nl))
+        costs = [layer_cost(L.dim_a, L.dim_g, rank, oversampling) for L in self.layers]
+        self.parts = [p for p in lpt_partition(costs, max(1, min(groups, nl))) if p]
+        ns = list(n_samples)
+        self.subs = []
+        for part in self.parts:
+            sub_ns = ns if len(ns) <= 1 else [ns[2 * l + w] for l in part for w in (0, 1)]
+            self.subs.append(BatchedStep([self.layers[l] for l in part], rank=rank, oversampling=oversampling,
+                                         power_iters=power_iters, method=method, n_samples=sub_ns, device=device,
+                                         factor_indices=[tags[2 * l + w] for l in part for w in (0, 1)]))
+        self.ctx = self.subs[0].ctx
+        self.streams = [torch.cuda.Stream(device=device) for _ in self.subs]
+        # views in the original order
+        self.dims, self.factors, self.samples, self.bases_t, self.dvals, self.ranks = [], [], [], [], [], []
+        self.grads, self.outs, self.mids = [None] * nl, [None] * nl, [None] * nl
+        self._owner = [None] * (2 * nl)
+        for s, (part, sub) in enumerate(zip(self.parts, self.subs)):
+            for i, l in enumerate(part):
+                self.grads[l], self.outs[l], self.mids[l] = sub.grads[i], sub.outs[i], sub.mids[i]
+                for w in (0, 1):
+                    self._owner[2 * l + w] = (s, 2 * i + w)
+        for f in range(2 * nl):
+            s, j = self._owner[f]
+            sub = self.subs[s]
+            self.dims.append(sub.dims[j])
+            self.factors.append(sub.factors[j])
+            self.samples.append(sub.samples[j] if sub.samples else None)
+            self.bases_t.append(sub.bases_t[j])
+            self.dvals.append(sub.dvals[j])
+            self.ranks.append(sub.ranks[j])
+
+    def _fan_out(self, fn):
+        torch = _torch()
+        main = torch.cuda.current_stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        joins = []
+        for sub, st in zip(self.subs, self.streams):
+            st.wait_event(fork)
+            with torch.cuda.stream(st):
+                fn(sub)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                joins.append(ev)
+        for ev in joins:
+            main.wait_event(ev)
+        self.ctx.sync_stream()
+
+    def ea_update(self, rho: float = 0.95, scale: float = 1.0):
+        self._fan_out(lambda s: s.ea_update(rho, scale))
+
+    def decompose(self, rng_root: int, step: int):
+        self._fan_out(lambda s: s.decompose(rng_root, step))
+
+    def precondition(self, lam: float):
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        self._fan_out(lambda s: s.precondition(lam))
+
+    def step(self, rng_root: int, step: int, lam: float, rho: float = 0.95, scale: float = 1.0):
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        self._fan_out(lambda s: s.step(rng_root, step, lam, rho, scale))
+
+    def lowrank(self, f: int) -> LowRankEig:
+        s, j = self._owner[f]
+        return self.subs[s].lowrank(j)

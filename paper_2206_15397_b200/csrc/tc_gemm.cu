@@ -674,7 +674,9 @@ void TcGemm::finalize() {
     nred_ = (int)red.size();
     // LPT over persistent CTAs: tile cost ~ K blocks * (n_tile + epilogue overhead)
     const int ntiles = (int)tiles_.size();
-    nctas_ = std::max(1, std::min(ntiles, kNumSMs));
+    int cap = kNumSMs;
+    if (const char* e = std::getenv("RKFAC_TC_MAX_CTAS")) cap = std::max(1, std::min(kNumSMs, std::atoi(e)));
+    nctas_ = std::max(1, std::min(ntiles, cap));
     std::vector<int> order(ntiles);
     std::iota(order.begin(), order.end(), 0);
     auto cost = [&](int i) {

@@ -365,3 +365,35 @@ def test_rank_deficient_ea_start_is_fast_and_exact(port, cuda):
     # FP32 ulps times sqrt(w) rather than to one
     assert orth_err(u) < 5e-5
     assert elapsed < 0.1, elapsed
+
+
+def test_streamed_step_is_bitwise_the_batched_step(cuda):
+    """Layer groups on separate streams (StreamedStep) give bitwise the single-plan result."""
+    import math
+
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    layers = [rk.LayerSpec(577, 64), rk.LayerSpec(300, 257), rk.LayerSpec(28, 64), rk.LayerSpec(513, 10)]
+    kw = dict(rank=40, oversampling=10, power_iters=2, method=rk.DecompMethod.SREVD, n_samples=[64], device=0)
+    one = rk.BatchedStep(layers, **kw)
+    two = rk.StreamedStep(layers, groups=2, **kw)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for f, d in enumerate(one.dims):
+        s = torch.arange(1, d + 1, device=cuda, dtype=torch.float32).pow(-1.0)
+        m = torch.randn(d, 64, device=cuda, generator=g) * s[:, None] / math.sqrt(64)
+        one.samples[f].copy_(m)
+        two.samples[f].copy_(m)
+    for l, L in enumerate(layers):
+        j = torch.randn(L.dim_g, L.dim_a, device=cuda, generator=g)
+        one.grads[l].copy_(j)
+        two.grads[l].copy_(j)
+    for k in range(3):
+        one.step(7, k, 0.1)
+        two.step(7, k, 0.1)
+    torch.cuda.synchronize()
+    for f in range(len(one.dims)):
+        assert torch.equal(one.factors[f], two.factors[f])
+        assert torch.equal(one.bases_t[f], two.bases_t[f]) and torch.equal(one.dvals[f], two.dvals[f])
+    for l in range(len(layers)):
+        assert torch.equal(one.outs[l], two.outs[l])
