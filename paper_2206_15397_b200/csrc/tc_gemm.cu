@@ -526,31 +526,64 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     }
 }
 
-// Deterministic split-K reduction (fixed slice order) + the full epilogue, flattened over every split problem's
-// elements (one pass; the slices of an element are loaded 4 at a time).
-__global__ void tc_reduce_kernel(const TcProb* __restrict__ probs, const TcRed* __restrict__ red, int nred,
-                                 long long total) {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
+// Deterministic split-K reduction (fixed slice order) + the full epilogue, one 32x32 output tile per block:
+// partials (column-major per slice) are summed with coalesced loads along m, the tile is staged in smem, and every
+// output plane leaves coalesced -- along m for transposed layouts, along n (read transposed) for row-major ones.
+__global__ void __launch_bounds__(256) tc_reduce_kernel(const TcProb* __restrict__ probs,
+                                                        const TcRed* __restrict__ red, int nred, long long total) {
+    __shared__ float tile[32][33];
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;  // 8 warps
+    for (long long tt = blockIdx.x; tt < total; tt += gridDim.x) {
         int lo = 0, hi = nred - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (red[mid].off <= e) lo = mid; else hi = mid - 1;
+            if (red[mid].off <= tt) lo = mid; else hi = mid - 1;
         }
         const TcProb& pr = probs[red[lo].prob];
-        const long long local = e - red[lo].off;
+        const int local = (int)(tt - red[lo].off);
+        const int tn = local / red[lo].tiles_m, tm = local - tn * red[lo].tiles_m;
+        const int m0 = tm * 32, n0 = tn * 32;
         const long long mn = (long long)pr.M * pr.N;
-        const float* part = pr.partial + local;
-        float s0 = part[0], s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int k = 1;
-        for (; k + 3 < pr.ksplit; k += 4) {  // fixed association: ((s0 + s1) + (s2 + s3)) per group of 4
-            const float a = part[k * mn], b = part[(k + 1) * mn], c = part[(k + 2) * mn], d = part[(k + 3) * mn];
-            s0 += a; s1 += b; s2 += c; s3 += d;
+        __syncthreads();  // previous tile's reads of `tile` are done
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int nl = wy + 8 * u, m = m0 + lane, n = n0 + nl;
+            float v = 0.f;
+            if (m < pr.M && n < pr.N) {
+                const float* part = pr.partial + (long long)n * pr.M + m;
+                float s0 = part[0], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                int k = 1;
+                for (; k + 3 < pr.ksplit; k += 4) {  // fixed association: ((s0 + s1) + (s2 + s3))
+                    const float a = part[k * mn], b = part[(k + 1) * mn], c = part[(k + 2) * mn],
+                                d = part[(k + 3) * mn];
+                    s0 += a; s1 += b; s2 += c; s3 += d;
+                }
+                for (; k < pr.ksplit; ++k) s0 += part[k * mn];
+                v = epi_value(pr, m, n, (s0 + s1) + (s2 + s3));
+            }
+            tile[nl][lane] = v;
         }
-        for (; k < pr.ksplit; ++k) s0 += part[k * mn];
-        const float s = (s0 + s1) + (s2 + s3);
-        const int n = (int)(local / pr.M), m = (int)(local - (long long)n * pr.M);  // partials are column-major
-        store_outputs(pr, m, n, epi_value(pr, m, n, s));
+        __syncthreads();
+#pragma unroll 1
+        for (int o = 0; o < 4; ++o) {
+            float* p = pr.o[o];
+            if (!p) continue;
+            const bool islo = pr.is_lo[o] != 0;
+            const long long ld = pr.ldo[o];
+            if (pr.to[o]) {  // p[n * ld + m]: along m
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int nl = wy + 8 * u, m = m0 + lane, n = n0 + nl;
+                    if (m < pr.M && n < pr.N) p[(long long)n * ld + m] = lo_or(tile[nl][lane], islo);
+                }
+            } else {  // p[m * ld + n]: along n
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int ml = wy + 8 * u, m = m0 + ml, n = n0 + lane;
+                    if (m < pr.M && n < pr.N) p[(long long)m * ld + n] = lo_or(tile[lane][ml], islo);
+                }
+            }
+        }
     }
 }
 
@@ -625,8 +658,9 @@ int TcGemm::add(const TcProblemDesc& d) {
     const int ntm = (int)ceil_div(d.M, kBM);
     const int mn_tiles = d.sym ? ntm * (ntm + 1) / 2 : ntm * ntn;
     int ks = d.ksplit;
-    if (ks <= 0) {  // split long-K problems with few output tiles: >= 8 CTAs per problem, >= 32 K blocks a slice
+    if (ks <= 0) {  // fixed per shape, so results never depend on the batch composition
         ks = 1;
+        // long-K problems with few output tiles: >= 8 CTAs per problem, >= 32 K blocks a slice
         while (mn_tiles * ks < 8 && p.kblocks / (2 * ks) >= 32) ks *= 2;
     }
     RKFAC_REQUIRE(!(d.sym && ks > 1), RKFAC_INVALID_ARGUMENT, "sym tc problem cannot be split");
@@ -667,8 +701,9 @@ void TcGemm::finalize() {
             p.partial = partials_.as<float>() + off;
             off += (size_t)p.ksplit * p.M * p.N;
             any_split_ = true;
-            red.push_back(TcRed{red_total_, (int)i});
-            red_total_ += (long long)p.M * p.N;
+            const int tm = (int)ceil_div(p.M, 32), tn = (int)ceil_div(p.N, 32);
+            red.push_back(TcRed{red_total_, (int)i, tm});
+            red_total_ += (long long)tm * tn;
         }
     }
     nred_ = (int)red.size();
@@ -720,7 +755,7 @@ void TcGemm::launch(cudaStream_t s) const {
     count_launch();
     RKFAC_CHECK_LAUNCH();
     if (any_split_) {
-        const int blocks = (int)std::min<long long>(ceil_div(red_total_, 256), kNumSMs * 8);
+        const int blocks = (int)std::min<long long>(red_total_, kNumSMs * 8);
         tc_reduce_kernel<<<blocks, 256, 0, s>>>(d_probs_.as<TcProb>(), d_red_.as<TcRed>(), nred_, red_total_);
         count_launch();
         RKFAC_CHECK_LAUNCH();

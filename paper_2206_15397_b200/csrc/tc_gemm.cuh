@@ -51,9 +51,9 @@ struct TcTile {
     int prob, m0, n0, kb0, kb1, slice, pad_[2];
 };
 
-struct TcRed {  // split-K reduction map: element offset of a split problem in the flattened reduction
+struct TcRed {  // split-K reduction map: first 32x32 output tile of a split problem in the flattened reduction
     long long off;
-    int prob;
+    int prob, tiles_m;
 };
 
 class TcGemm {
