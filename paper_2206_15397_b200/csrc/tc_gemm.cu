@@ -32,11 +32,12 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 16;          // floats per K block (64 bytes per row => SWIZZLE_64B)
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kMaxBN = 256;
-constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB
+constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB (one 128-row A sub-tile)
 constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
-constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;  // 48 KB
+// stage: [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo]; A1 is used by paired tiles (256 rows sharing the B tile)
+constexpr int kStageBytes = 4 * kATileBytes + 2 * kBTileBytes;  // 64 KB
 constexpr int kThreads = 192;
 
 struct __align__(8) SmemBarriers {
@@ -386,16 +387,20 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
                 const CUtensorMap* mp = maps + 4 * tl.prob;
-                const uint32_t bytes = 2u * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
+                const uint32_t bytes = (tl.pair ? 4u : 2u) * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
                     unsigned char* st = smem + stage * kStageBytes;
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
                     tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + 2 * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
-                    tma_load_2d(st + 2 * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    if (tl.pair) {
+                        tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, tl.m0 + kBM);
+                        tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
+                    }
+                    tma_load_2d(st + 4 * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 4 * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -405,48 +410,65 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            int it = 0;
-            for (int t = t_begin; t < t_end; ++t, ++it) {
+            int rr = 0;                     // next accumulator slot for a single tile
+            uint32_t uses[2] = {0u, 0u};    // completed uses of each slot (parity of its barriers)
+            for (int t = t_begin; t < t_end; ++t) {
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
-                mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
+                const int nsub = tl.pair ? 2 : 1;
+                const int slot0 = tl.pair ? 0 : rr;
+                for (int sub = 0; sub < nsub; ++sub) {
+                    const int a = slot0 + sub;
+                    mbar_wait(&bars->tmem_empty[a], (uses[a] & 1u) ^ 1u);
+                }
                 tc_fence_after();
-                const uint32_t tmem_d = tmem_base + acc * kMaxBN;
                 const uint32_t idesc = idesc_tf32(pr.n_tile);
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
-                    const uint32_t a_hi = st, a_lo = st + kATileBytes;
-                    const uint32_t b_hi = st + 2 * kATileBytes, b_lo = b_hi + kBTileBytes;
+                    const uint32_t b_hi = st + 4 * kATileBytes, b_lo = b_hi + kBTileBytes;
+                    for (int sub = 0; sub < nsub; ++sub) {
+                        const uint32_t tmem_d = tmem_base + (slot0 + sub) * kMaxBN;
+                        const uint32_t a_hi = st + sub * kATileBytes, a_lo = st + (2 + sub) * kATileBytes;
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 8; ++kk) {
-                        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
-                        const uint32_t first = (kb == tl.kb0 && kk == 0) ? 0u : 1u;
-                        mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
-                        mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
-                        mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc, 1u);
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
+                            const uint32_t first = (kb == tl.kb0 && kk == 0) ? 0u : 1u;
+                            mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
+                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
+                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc, 1u);
+                        }
                     }
                     mma_commit(&bars->empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&bars->tmem_full[acc]);
+                for (int sub = 0; sub < nsub; ++sub) {
+                    mma_commit(&bars->tmem_full[slot0 + sub]);
+                    ++uses[slot0 + sub];
+                }
+                if (!tl.pair) rr ^= 1;
             }
         }
     } else {
         // ---------------- epilogue ----------------
         const int q = warp % 4;  // TMEM lane quadrant this warp may access
-        int it = 0;
-        for (int t = t_begin; t < t_end; ++t, ++it) {
-            const TcTile tl = tiles[t];
+        int rr = 0;
+        uint32_t uses[2] = {0u, 0u};
+        for (int t = t_begin; t < t_end; ++t) {
+          const TcTile tl = tiles[t];
+          const int nsub = tl.pair ? 2 : 1;
+          const int slot0 = tl.pair ? 0 : rr;
+          if (!tl.pair) rr ^= 1;
+          for (int sub = 0; sub < nsub; ++sub) {
             const TcProb& pr = probs[tl.prob];
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            const int mbase = tl.m0 + q * 32;
+            const int acc = slot0 + sub;
+            const uint32_t acc_phase = uses[acc] & 1u;
+            ++uses[acc];
+            const int m0s = tl.m0 + sub * kBM;  // this sub-tile's first row
+            const int mbase = m0s + q * 32;
             const int m = mbase + lane;
-            const bool diag = pr.sym && tl.m0 == tl.n0;
+            const bool diag = pr.sym && m0s == tl.n0;
             const int nlim = min(pr.N, tl.n0 + pr.n_tile);
             float (*tile)[kTP] = stage_tiles[warp - 2];
             // prefetch the first Cin chunk (row-major axpy input, e.g. the EA factor) before the accumulator is ready
@@ -517,6 +539,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             }
             tc_fence_before();
             mbar_arrive(&bars->tmem_empty[acc]);
+          }
         }
     }
     __syncthreads();
@@ -673,11 +696,15 @@ int TcGemm::add(const TcProblemDesc& d) {
     for (int s = 0; s < ks; ++s) {
         const int kb0 = s * kper, kb1 = std::min(p.kblocks, kb0 + kper);
         if (kb0 >= kb1) continue;
+        // tall problems (>= 8 row tiles, unsplit, not symmetric): pairs of row tiles share each B tile (halves the
+        // L2->SM traffic of B, the re-read operand); the accumulation order per element is unchanged (bitwise)
+        const bool pairs = !d.sym && ks == 1 && ntm >= 8;
         for (int tn = 0; tn < ntn; ++tn)
-            for (int tm = 0; tm < ntm; ++tm) {
+            for (int tm = 0; tm < ntm; tm += (pairs ? 2 : 1)) {
                 if (d.sym && tn < tm) continue;
                 TcTile t{};
                 t.prob = prob; t.m0 = tm * kBM; t.n0 = tn * per; t.kb0 = kb0; t.kb1 = kb1; t.slice = s;
+                t.pair = (pairs && tm + 1 < ntm) ? 1 : 0;
                 tiles_.push_back(t);
             }
     }
@@ -716,7 +743,8 @@ void TcGemm::finalize() {
     std::iota(order.begin(), order.end(), 0);
     auto cost = [&](int i) {
         const TcTile& t = tiles_[i];
-        return (double)(t.kb1 - t.kb0) * (probs_[t.prob].n_tile + 16) + 4.0 * probs_[t.prob].n_tile;
+        return (t.pair ? 2.0 : 1.0) * ((double)(t.kb1 - t.kb0) * (probs_[t.prob].n_tile + 16) +
+                                        4.0 * probs_[t.prob].n_tile);
     };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
     std::vector<double> load(nctas_, 0.0);

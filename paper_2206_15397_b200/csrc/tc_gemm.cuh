@@ -48,7 +48,7 @@ struct TcProb {  // device copy
 };
 
 struct TcTile {
-    int prob, m0, n0, kb0, kb1, slice, pad_[2];
+    int prob, m0, n0, kb0, kb1, slice, pair, pad_;  // pair: rows m0 .. m0+255 as two accumulators sharing B
 };
 
 struct TcRed {  // split-K reduction map: first 32x32 output tile of a split problem in the flattened reduction
