@@ -32,17 +32,25 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 16;          // floats per K block (64 bytes per row => SWIZZLE_64B)
-constexpr int kStages = 3;
+constexpr int kMaxStages = 4;
 constexpr int kMaxBN = 256;
 constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB (one 128-row A sub-tile)
 constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
-// stage: [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo]; A1 is used by paired tiles (256 rows sharing the B tile)
-constexpr int kStageBytes = 4 * kATileBytes + 2 * kBTileBytes;  // 64 KB
+// Two shared-memory configurations (same ~192 KB):
+//   single tiles: 4 stages of [A hi][A lo][B hi][B lo] = 48 KB
+//   paired tiles: 3 stages of [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo] = 64 KB (256 rows share the B tile)
+template <bool kPair>
+struct StageCfg {
+    static constexpr int kSub = kPair ? 2 : 1;
+    static constexpr int kStages = kPair ? 3 : 4;
+    static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTileBytes;
+};
+constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 4 * 48 KB
 constexpr int kThreads = 192;
 
 struct __align__(8) SmemBarriers {
-    uint64_t full[kStages];
-    uint64_t empty[kStages];
+    uint64_t full[kMaxStages];
+    uint64_t empty[kMaxStages];
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
     uint32_t tmem_base;
@@ -345,15 +353,19 @@ __device__ __forceinline__ void chunk_store_pair(const float (&v)[32], float* ph
 }
 
 // ------------------------------------------------------------------------------------------------ kernel
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__ maps,
                const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
+    constexpr int kStages = StageCfg<kPair>::kStages;
+    constexpr int kStageBytes = StageCfg<kPair>::kStageBytes;
+    constexpr int kSub = StageCfg<kPair>::kSub;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
-    SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStages * kStageBytes);
+    SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStagesBytesMax);
     float (*stage_tiles)[32][36] =
-        reinterpret_cast<float (*)[32][36]>(smem + kStages * kStageBytes + kBarrierBytes);
+        reinterpret_cast<float (*)[32][36]>(smem + kStagesBytesMax + kBarrierBytes);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int t_begin = cta_begin[blockIdx.x], t_end = cta_begin[blockIdx.x + 1];
 
@@ -394,13 +406,13 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
                     tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + 2 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
-                    if (tl.pair) {
+                    tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    if (kPair && tl.pair) {
                         tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, tl.m0 + kBM);
                         tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
                     }
-                    tma_load_2d(st + 4 * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
-                    tma_load_2d(st + 4 * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kSub * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -415,8 +427,8 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             for (int t = t_begin; t < t_end; ++t) {
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
-                const int nsub = tl.pair ? 2 : 1;
-                const int slot0 = tl.pair ? 0 : rr;
+                const int nsub = (kPair && tl.pair) ? 2 : 1;
+                const int slot0 = (kPair && tl.pair) ? 0 : rr;
                 for (int sub = 0; sub < nsub; ++sub) {
                     const int a = slot0 + sub;
                     mbar_wait(&bars->tmem_empty[a], (uses[a] & 1u) ^ 1u);
@@ -427,10 +439,10 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     mbar_wait(&bars->full[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
-                    const uint32_t b_hi = st + 4 * kATileBytes, b_lo = b_hi + kBTileBytes;
+                    const uint32_t b_hi = st + 2 * kSub * kATileBytes, b_lo = b_hi + kBTileBytes;
                     for (int sub = 0; sub < nsub; ++sub) {
                         const uint32_t tmem_d = tmem_base + (slot0 + sub) * kMaxBN;
-                        const uint32_t a_hi = st + sub * kATileBytes, a_lo = st + (2 + sub) * kATileBytes;
+                        const uint32_t a_hi = st + sub * kATileBytes, a_lo = st + (kSub + sub) * kATileBytes;
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
@@ -447,7 +459,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     mma_commit(&bars->tmem_full[slot0 + sub]);
                     ++uses[slot0 + sub];
                 }
-                if (!tl.pair) rr ^= 1;
+                if (!(kPair && tl.pair)) rr ^= 1;
             }
         }
     } else {
@@ -457,9 +469,9 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         uint32_t uses[2] = {0u, 0u};
         for (int t = t_begin; t < t_end; ++t) {
           const TcTile tl = tiles[t];
-          const int nsub = tl.pair ? 2 : 1;
-          const int slot0 = tl.pair ? 0 : rr;
-          if (!tl.pair) rr ^= 1;
+          const int nsub = (kPair && tl.pair) ? 2 : 1;
+          const int slot0 = (kPair && tl.pair) ? 0 : rr;
+          if (!(kPair && tl.pair)) rr ^= 1;
           for (int sub = 0; sub < nsub; ++sub) {
             const TcProb& pr = probs[tl.prob];
             const int acc = slot0 + sub;
@@ -713,6 +725,29 @@ int TcGemm::add(const TcProblemDesc& d) {
 }
 
 void TcGemm::finalize() {
+    // Paired tiles halve the B traffic but also the number of schedulable units: keep them only when the paired
+    // units still fill every SM (pairing never changes the arithmetic, so this may depend on the batch).
+    {
+        long long units = 0, paired_units = (long long)tiles_.size();
+        for (const auto& t : tiles_) units += t.pair ? 2 : 1;
+        if (paired_units < kNumSMs) {
+            std::vector<TcTile> split;
+            split.reserve((size_t)units);
+            for (const auto& t : tiles_) {
+                TcTile a = t;
+                a.pair = 0;
+                split.push_back(a);
+                if (t.pair) {
+                    a.m0 = t.m0 + kBM;
+                    split.push_back(a);
+                }
+            }
+            tiles_.swap(split);
+        }
+        // the 3 x 64 KB configuration also measured faster for the symmetric EA update (0.62 vs 0.84 ms, VGG16)
+        paired_ = false;
+        for (const auto& t : tiles_) paired_ = paired_ || t.pair || probs_[t.prob].sym;
+    }
     // split-K partial buffers
     size_t total = 0;
     for (auto& p : probs_)
@@ -772,14 +807,15 @@ void TcGemm::finalize() {
     up(d_red_, red.data(), sizeof(TcRed) * red.size());
 }
 
-size_t TcGemm::smem_bytes() { return (size_t)kStages * kStageBytes + kBarrierBytes + kStageTileBytes + 1024; }
+size_t TcGemm::smem_bytes() { return (size_t)kStagesBytesMax + kBarrierBytes + kStageTileBytes + 1024; }
 
 void TcGemm::launch(cudaStream_t s) const {
     if (tiles_.empty()) return;
     const size_t smem = smem_bytes();
-    RKFAC_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tc_gemm_kernel<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(),
-                                                  d_tiles_.as<TcTile>(), d_begin_.as<int>());
+    auto k = paired_ ? tc_gemm_kernel<true> : tc_gemm_kernel<false>;
+    RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(), d_tiles_.as<TcTile>(),
+                                     d_begin_.as<int>());
     count_launch();
     RKFAC_CHECK_LAUNCH();
     if (any_split_) {
