@@ -357,6 +357,7 @@ template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__ maps,
                const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
+    __shared__ TcProb s_pr[4];  // per epilogue warp
     constexpr int kStages = StageCfg<kPair>::kStages;
     constexpr int kStageBytes = StageCfg<kPair>::kStageBytes;
     constexpr int kSub = StageCfg<kPair>::kSub;
@@ -472,8 +473,16 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
           const int nsub = (kPair && tl.pair) ? 2 : 1;
           const int slot0 = (kPair && tl.pair) ? 0 : rr;
           if (!(kPair && tl.pair)) rr ^= 1;
+          // the problem descriptor in this warp's shared-memory slot: its fields are re-read in every chunk, and
+          // from global memory the compiler must reload them after each epilogue store (possible aliasing)
+          {
+              const int* src = reinterpret_cast<const int*>(&probs[tl.prob]);
+              int* dst = reinterpret_cast<int*>(&s_pr[warp - 2]);
+              for (int i = lane; i < (int)(sizeof(TcProb) / sizeof(int)); i += 32) dst[i] = src[i];
+              __syncwarp();
+          }
           for (int sub = 0; sub < nsub; ++sub) {
-            const TcProb& pr = probs[tl.prob];
+            const TcProb& pr = s_pr[warp - 2];
             const int acc = slot0 + sub;
             const uint32_t acc_phase = uses[acc] & 1u;
             ++uses[acc];
