@@ -20,6 +20,9 @@
 //   inverse    all 32x32 diagonal blocks inverted concurrently (one warp each), then recursive doubling over block
 //              segments, B <- -C^{-1} B A^{-1}, as passes of register tiles (log2(w/32) levels, 4 barriers each).
 #include <cmath>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "kernels.cuh"
 
@@ -47,6 +50,7 @@ constexpr int kCholThreads = 512;  // 128-register budget: the unrolled 32-wide 
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __host__ __device__ __forceinline__ int rup4(int x) { return (x + 3) & ~3; }
+__host__ __device__ __forceinline__ int rup8(int x) { return (x + 7) & ~7; }
 
 // Offset of row i in the padded packed layout: sum_{t<i} rup4(t+1) plus 4 skew elements after every block of 4
 // rows.  rup4(t+1) for t = 4a+b is 4a+4, so block a starts at 8a(a+1); without the skew the rows 4a (the first rows
@@ -538,6 +542,423 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
     CHOL_PHASE(57);
 }
 
+// ------------------------------------------------------------------------------ Cholesky-inverse on a CTA cluster
+// cholinv_cluster_kernel: the same G = L L^T, Linv = L^{-1} (same deficiency semantics) spread over a cluster of 4
+// CTAs per factor.  L itself is never stored: the inverse is accumulated by the same right-looking sweep, so there is
+// no separate inversion phase.  32-row blocks are owned in snake order (0,1,2,3,3,2,1,0,0,...), each owned row i kept
+// in the owner's shared memory as ONE row of (block+1)*32 entries: columns left of the current panel hold the
+// partial inverse row R_i = e_i - sum_{c<=b} L_ic X_c, columns right of it the trailing Schur complement.
+// Step b (panel of block b, J0 = 32b):
+//   1. owner(b): L_bb = chol(A_bb) by one warp (pivot chain on shuffles), then X_b = L_bb^{-1} [R_b | I] by one
+//      thread per column -- X_b is the final block row b of Linv (written to global at once);        barrier
+//   2. all: X_b copied from the owner (distributed shared memory), panel rows of the owned rows below,
+//      P_i = A_i(:, J0:J0+32) L_bb^{-T} (L_bb^{-1} is X_b's last 32 columns), pushed to every CTA's panel;  barrier
+//   3. all, owned rows below block b, 4x4 register tiles with k-major operands (conflict-free LDS.128):
+//      trailing A_ic -= P_i . P_c (J0+32 <= c <= i) and inverse R_i(:, 0:J0+32) -= P_i X_b.
+// Two cluster barriers per 32 columns (16 for w = 230) instead of the single CTA's serial TRSM and log-depth
+// inversion; every product has a fixed order (deterministic).
+constexpr int kCC = 4;
+constexpr int kCcThreads = 384;
+constexpr int kCcMaxBlk = 16;
+
+__host__ __device__ __forceinline__ int cc_owner(int b) {
+    const int r = b % (2 * kCC);
+    return r < kCC ? r : 2 * kCC - 1 - r;
+}
+__host__ __device__ __forceinline__ int cc_pitch(int b) { return (b + 1) * kNB + 4; }  // odd in 16-byte units
+
+__host__ __device__ inline int cc_rows_elems(int n, int q) {
+    const int nblk = (n + kNB - 1) / kNB;
+    int e = 0;
+    for (int b = 0; b < nblk; ++b)
+        if (cc_owner(b) == q) e += min(kNB, n - b * kNB) * cc_pitch(b);
+    return e;
+}
+
+__host__ __device__ inline size_t cc_smem_bytes(int n, int es) {
+    int rows = 0;
+    for (int q = 0; q < kCC; ++q) rows = max(rows, cc_rows_elems(n, q));
+    rows = (rows + 3) & ~3;
+    const int np = rup8(n) + 4, xbp = rup8(n) + 4, lp = kNB + 4;  // odd multiples of 16 bytes
+    size_t b = (size_t)es * ((size_t)rows + (size_t)kNB * np + (size_t)kNB * xbp + (size_t)kNB * lp + 3 * kNB);
+    b = (b + 15) & ~(size_t)15;
+    b += 4 * (size_t)rup4(n) + (size_t)rup4(n) + 16 + 64;  // diag0 (float), defic, flags
+    return (b + 15) & ~(size_t)15;
+}
+
+__device__ __forceinline__ void cc_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <class TG, class T>
+__global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
+    cholinv_cluster_kernel(const CholDesc* __restrict__ descs, double tol) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int q = (int)cluster.block_rank();
+    const CholDesc& cd = descs[blockIdx.x / kCC];
+    const int n = cd.w, nblk = (n + kNB - 1) / kNB;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int np = rup8(n) + 4, xbp = rup8(n) + 4, lp = kNB + 4;  // odd multiples of 16 bytes
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* rows = reinterpret_cast<T*>(smem_raw);
+    // the row storage differs per CTA; everything after it sits at the same offset in every CTA (pushed remotely)
+    int mxrows = 0;
+    for (int qq = 0; qq < kCC; ++qq) mxrows = max(mxrows, cc_rows_elems(n, qq));
+    T* panel = rows + ((mxrows + 3) & ~3);  // k-major [kNB][np]: panel[k][i] = P_ik
+    T* xb = panel + kNB * np;      // X_b, k-major [kNB][xbp]
+    T* lbbT = xb + kNB * xbp;      // L_bb transposed: lbbT[c][i] = L_ic
+    T* dinv = lbbT + kNB * lp;     // 1 / L_kk (0 for a deficient pivot)
+    T* colbuf = dinv + kNB;        // 2 x kNB column broadcast of the factorisation
+    float* diag0 = reinterpret_cast<float*>(
+        reinterpret_cast<unsigned char*>(smem_raw) +
+        ((sizeof(T) * ((size_t)(panel - rows) + (size_t)kNB * np + (size_t)kNB * xbp + (size_t)kNB * lp + 3 * kNB) +
+          15) & ~(size_t)15));
+    unsigned char* defic = reinterpret_cast<unsigned char*>(diag0 + rup4(n));
+    int* cflags = reinterpret_cast<int*>(defic + ((rup4(n) + 15) & ~15));  // [kCC] any-deficiency per CTA (CTA 0)
+    __shared__ int boff[kCcMaxBlk];
+    __shared__ int any_defic;
+    const T tolT = T(tol);
+
+    // ---- layout of the owned blocks, zeroed panel / X_b buffers, owned rows of G (lower triangle)
+    if (tid == 0) {
+        int e = 0;
+        for (int b = 0; b < nblk; ++b) {
+            if (cc_owner(b) == q) { boff[b] = e; e += min(kNB, n - b * kNB) * cc_pitch(b); }
+            else boff[b] = -1;
+        }
+        any_defic = 0;
+    }
+    for (int i = tid; i < kNB * np; i += kCcThreads) panel[i] = T(0);
+    for (int i = tid; i < kNB * xbp; i += kCcThreads) xb[i] = T(0);
+    __syncthreads();
+    const TG* G = static_cast<const TG*>(cd.G);
+    for (int b = 0; b < nblk; ++b) {
+        if (boff[b] < 0) continue;
+        const int J0 = b * kNB, nb = min(kNB, n - J0), pb = cc_pitch(b);
+        T* rb = rows + boff[b];
+        for (int r = warp; r < nb; r += kCcThreads / 32) {
+            const int i = J0 + r;
+            for (int j = lane; j < pb; j += 32) rb[r * pb + j] = (j <= i) ? T(G[(long long)i * cd.ldg + j]) : T(0);
+            if (lane == 0) { diag0[i] = (float)G[(long long)i * cd.ldg + i]; defic[i] = 0; }
+        }
+    }
+    CHOL_PHASE(0);
+    cluster.sync();  // every CTA runs: distributed shared memory may be accessed
+    CHOL_PHASE(1);
+
+    T* out = static_cast<T*>(cd.Linv);
+    float* lo = static_cast<float*>(cd.Linv_lo);
+    const bool vec_out = (cd.ldl & 3) == 0 && (((uintptr_t)out) & (4 * sizeof(T) - 1)) == 0 &&
+                         (!lo || (((uintptr_t)lo) & 15) == 0);
+
+    // 32x32 diagonal block fb of the owner, one warp: L_bb into lbbT (transposed), 1/L_kk into dinv
+    auto factor_block = [&](int fb) {
+        const int J0 = fb * kNB, nb = min(kNB, n - J0), pb = cc_pitch(fb);
+        const T* rb = rows + boff[fb];
+            T a[kNB];
+            const int rl = min(lane, nb - 1);
+#pragma unroll
+            for (int c4 = 0; c4 < kNB; c4 += 4) {
+                T v4[4];
+                ld4(rb + rl * pb + J0 + c4, v4);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[c4 + u] = (lane < nb && c4 + u <= lane) ? v4[u] : T(0);
+            }
+            // right-looking, lane = row: the pivot and the next pivot's multiplier by shuffle, the rest of the
+            // column through shared memory (double-buffered, one __syncwarp per step); FP32 applies that rest one
+            // step late (software pipelined: the shared-memory round trip leaves the pivot chain)
+            T tp[kNB];
+            auto step = [&](int k, int nbv, bool defer) {
+                const T piv = __shfl_sync(0xffffffffu, a[k], k);
+                const T g = T(diag0[J0 + k]);
+                const bool def = !(piv > tolT * g) || g == T(0);
+                const T inv = def ? T(0) : rsqrt_t(piv);
+                const T lkk = def ? T(1) : piv * inv;
+                a[k] = lane == k ? lkk : (lane > k ? a[k] * inv : a[k]);
+                if (lane == 0) dinv[k] = inv;
+                if (def && lane == 0) { defic[J0 + k] = 1; any_defic = 1; }
+                if (k + 1 < nbv) {
+                    const T tn = __shfl_sync(0xffffffffu, a[k], k + 1);
+                    T* cb = colbuf + (k & 1) * kNB;
+                    cb[lane] = a[k];
+                    __syncwarp();
+                    if (defer) {
+                        T tc[kNB];
+#pragma unroll
+                        for (int q4 = (k + 2) & ~3; q4 < kNB; q4 += 4) {
+                            T v4[4];
+                            ld4(cb + q4, v4);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) tc[q4 + u] = v4[u];
+                        }
+                        if (k >= 1) {
+#pragma unroll
+                            for (int j = k + 1; j < kNB; ++j) a[j] -= a[k - 1] * tp[j];
+                        }
+                        a[k + 1] -= a[k] * tn;
+#pragma unroll
+                        for (int j = k + 2; j < kNB; ++j) tp[j] = tc[j];
+                    } else {
+                        a[k + 1] -= a[k] * tn;
+#pragma unroll
+                        for (int q4 = (k + 2) & ~3; q4 < kNB; q4 += 4) {
+                            T v4[4];
+                            ld4(cb + q4, v4);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (q4 + u >= k + 2) a[q4 + u] -= a[k] * v4[u];
+                        }
+                    }
+                } else if (defer && k >= 1) {
+#pragma unroll
+                    for (int j = k + 1; j < kNB; ++j) a[j] -= a[k - 1] * tp[j];
+                }
+            };
+            constexpr bool kDefer = sizeof(T) == 4;
+            if (nb == kNB) {
+#pragma unroll
+                for (int k = 0; k < kNB; ++k) step(k, kNB, kDefer);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kNB; ++k)
+                    if (k < nb) step(k, nb, false);
+            }
+#pragma unroll
+            for (int c = 0; c < kNB; ++c) lbbT[c * lp + lane] = (lane < nb && c <= lane) ? a[c] : T(0);
+    };
+    // block row b of Linv is final: store it (rows of deficient pivots are zero) and its deficiency flags
+    auto store_block = [&](int sb, int w0) {  // by warps w0 ..
+        const int J0 = sb * kNB, nb = min(kNB, n - J0), pb = cc_pitch(sb);
+        const T* rb = rows + boff[sb];
+        for (int r = warp - w0; r < nb; r += kCcThreads / 32 - w0) {
+            const int i = J0 + r;
+            const T* row = rb + r * pb;
+            const int len = min(rup4(i + 1), (int)cd.ldl);
+            const bool z = defic[i];
+            if (vec_out) {
+                for (int c = lane * 4; c < len; c += 128) {
+                    T v[4];
+                    ld4(row + c, v);
+                    if (z) v[0] = v[1] = v[2] = v[3] = T(0);
+                    T* o = out + (long long)i * cd.ldl + c;
+                    if constexpr (sizeof(T) == 4) {
+                        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+                    } else {
+                        reinterpret_cast<double2*>(o)[0] = make_double2(v[0], v[1]);
+                        reinterpret_cast<double2*>(o)[1] = make_double2(v[2], v[3]);
+                    }
+                    if (lo) {
+                        float f[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) { const float x = (float)v[u]; f[u] = x - tf32_trunc(x); }
+                        *reinterpret_cast<float4*>(lo + (long long)i * cd.ldl + c) =
+                            make_float4(f[0], f[1], f[2], f[3]);
+                    }
+                }
+            } else {
+                for (int j = lane; j < len; j += 32) {
+                    const T v = z ? T(0) : row[j];
+                    out[(long long)i * cd.ldl + j] = v;
+                    if (lo) {
+                        const float f = (float)v;
+                        lo[(long long)i * cd.ldl + j] = f - tf32_trunc(f);
+                    }
+                }
+            }
+            if (lane == 0) cd.flags[i] = z;
+        }
+    };
+
+    for (int b = 0; b < nblk; ++b) {
+        const int J0 = b * kNB, nb = min(kNB, n - J0), own = cc_owner(b);
+        const int ncols = rup4(J0 + nb);  // columns of X_b (lower triangle, zero padded to a multiple of 4)
+        // ------------------------------------------------ 1. owner: factor the diagonal block, X_b = L_bb^-1 [R_b|I]
+        if (own == q) {
+            const int pb = cc_pitch(b);
+            T* rb = rows + boff[b];
+            if (b == 0 && warp == 0) factor_block(0);  // later blocks were factored during the previous step
+            __syncthreads();
+            CHOL_PHASE(30 + b);
+            // X_b = L_bb^{-1} [R_b(:, 0:J0) | I]: one thread per column, forward substitution in registers
+            for (int c = tid; c < ncols; c += kCcThreads) {
+                T acc[kNB];
+#pragma unroll
+                for (int i = 0; i < kNB; ++i)
+                    acc[i] = (i < nb) ? (c < J0 ? rb[i * pb + c] : (c - J0 == i ? T(1) : T(0))) : T(0);
+#pragma unroll
+                for (int k = 0; k < kNB; ++k) {
+                    const T x = acc[k] * dinv[k];
+                    acc[k] = x;
+#pragma unroll
+                    for (int i4 = (k + 1) & ~3; i4 < kNB; i4 += 4) {
+                        T l4[4];
+                        ld4(lbbT + k * lp + i4, l4);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i4 + u > k) acc[i4 + u] -= l4[u] * x;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < kNB; ++i)
+                    if (i < nb) rb[i * pb + c] = acc[i];
+            }
+            __syncthreads();
+            CHOL_PHASE(40 + b);
+            if (b + 1 == nblk) store_block(b, 0);
+        }
+        CHOL_PHASE(2 + 3 * b);
+        if (b + 1 == nblk) break;
+        cc_barrier();  // (1) X_b published
+        // ------------------------------------------------ 2. X_b from the owner; panel rows of the owned rows below
+        {
+            const T* src = cluster.map_shared_rank(rows, own);
+            // the owner's block-b offset: recomputed (boff is per CTA)
+            int ob = 0;
+            for (int bb = 0; bb < b; ++bb)
+                if (cc_owner(bb) == own) ob += min(kNB, n - bb * kNB) * cc_pitch(bb);
+            const int pb = cc_pitch(b);
+            const int c4n = ncols / 4;
+            for (int t = tid; t < nb * c4n; t += kCcThreads) {
+                const int r = t / c4n, c = (t - r * c4n) * 4;
+                T v[4];
+                ld4(src + ob + r * pb + c, v);
+                st4(xb + r * xbp + c, v[0], v[1], v[2], v[3]);
+            }
+        }
+        __syncthreads();
+        CHOL_PHASE(50 + b);
+        // owned rows below block b: thread = (4 rows, one panel column k), one 16-byte store into every CTA
+        for (int gbase = tid >> 5;; gbase += kCcThreads / 32) {
+            int g = gbase, ob = b + 1;
+            for (; ob < nblk; ++ob) {
+                if (boff[ob] < 0) continue;
+                const int G4 = (min(kNB, n - ob * kNB) + 3) / 4;
+                if (g < G4) break;
+                g -= G4;
+            }
+            if (ob >= nblk) break;
+            const int k = lane, pbo = cc_pitch(ob), nbo = min(kNB, n - ob * kNB);
+            const T* ar = rows + boff[ob] + g * 4 * pbo + J0;
+            const T* xr = xb + k * xbp + J0;
+            T acc[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+            for (int m4 = 0; m4 < kNB; m4 += 4) {
+                T x4[4];
+                ld4(xr + m4, x4);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (g * 4 + u < nbo) {
+                        T a4[4];
+                        ld4(ar + u * pbo + m4, a4);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) acc[u] += a4[m] * x4[m];
+                    }
+                }
+            }
+            const int i0 = ob * kNB + g * 4;
+#pragma unroll
+            for (int r = 0; r < kCC; ++r) st4(cluster.map_shared_rank(panel, r) + k * np + i0, acc[0], acc[1], acc[2], acc[3]);
+        }
+        CHOL_PHASE(3 + 3 * b);
+        cc_barrier();  // (2) panel complete in every CTA
+        // ------------------------------------------------ 3. trailing update and inverse update of the owned rows
+        {
+            // row groups of 4 owned rows below block b; group at row i0 has i0/4 + 1 column tiles (0 .. i0)
+            int total = 0;
+            for (int ob = b + 1; ob < nblk; ++ob) {
+                if (boff[ob] < 0) continue;
+                const int G4 = (min(kNB, n - ob * kNB) + 3) / 4;
+                total += G4 * (ob * 8 + 1) + G4 * (G4 - 1) / 2;
+            }
+            const int jb = J0 + kNB;  // first trailing column
+            // look-ahead: the owner of block b+1 updates that block's diagonal tiles first, then one warp factors it
+            // while the others finish the update
+            const bool ahead = cc_owner(b + 1) == q;
+            auto tile = [&](int t, bool& diag_next, int& obo, int& go, int& c0o) {
+                int rem = t, ob = b + 1, g = 0;
+                for (; ob < nblk; ++ob) {
+                    if (boff[ob] < 0) continue;
+                    const int G4 = (min(kNB, n - ob * kNB) + 3) / 4;
+                    const int tiles = G4 * (ob * 8 + 1) + G4 * (G4 - 1) / 2;
+                    if (rem < tiles) break;
+                    rem -= tiles;
+                }
+                for (;; ++g) {
+                    const int tg = ob * 8 + g + 1;
+                    if (rem < tg) break;
+                    rem -= tg;
+                }
+                obo = ob; go = g; c0o = rem * 4;
+                diag_next = ob == b + 1 && c0o >= jb;
+            };
+            auto run = [&](int ob, int g, int c0) {
+                const int i0 = ob * kNB + g * 4;
+                const int pbo = cc_pitch(ob);
+                T* rr = rows + boff[ob] + g * 4 * pbo;
+                const bool inv_tile = c0 < jb;
+                const T* bop = inv_tile ? (xb + c0) : (panel + c0);
+                const int bld = inv_tile ? xbp : np;
+                T acc[4][4] = {};
+#pragma unroll 8
+                for (int k = 0; k < kNB; ++k) {  // nb == kNB: every block but the last has a trailing update
+                    T av[4], bv[4];
+                    ld4(panel + k * np + i0, av);
+                    ld4(bop + k * bld, bv);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * bv[v];
+                }
+                const bool fresh = c0 >= J0 && c0 < jb;  // panel columns become inverse columns: old value 0
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (i0 + u >= n) continue;
+                    T* w = rr + u * pbo + c0;
+                    T o4[4] = {T(0), T(0), T(0), T(0)};
+                    if (!fresh) ld4(w, o4);
+                    st4(w, o4[0] - acc[u][0], o4[1] - acc[u][1], o4[2] - acc[u][2], o4[3] - acc[u][3]);
+                }
+            };
+            if (ahead) {
+                const int G4 = (min(kNB, n - (b + 1) * kNB) + 3) / 4;
+                const int nd = G4 * (G4 + 1) / 2;  // diagonal tiles of block b+1
+                for (int t = tid; t < nd; t += kCcThreads) {
+                    int g = 0, rem = t;
+                    while (rem > g) { rem -= g + 1; ++g; }
+                    run(b + 1, g, jb + rem * 4);
+                }
+                __syncthreads();
+                if (warp == 0) factor_block(b + 1);
+            }
+            if (!ahead || warp > 0) {
+                const int t0 = ahead ? tid - 32 : tid, nt = ahead ? kCcThreads - 32 : kCcThreads;
+                for (int t = t0; t < total; t += nt) {
+                    bool dn;
+                    int ob, g, c0;
+                    tile(t, dn, ob, g, c0);
+                    if (ahead && dn) continue;
+                    run(ob, g, c0);
+                }
+                // block row b of Linv: stored off the critical path (not by the warp factoring block b+1)
+                if (own == q) store_block(b, ahead ? 1 : 0);
+            }
+        }
+        __syncthreads();
+        CHOL_PHASE(4 + 3 * b);
+    }
+    // ---- any-deficiency flag: gathered in CTA 0
+    if (tid == 0) cluster.map_shared_rank(cflags, 0)[q] = any_defic;
+    cc_barrier();
+    if (q == 0 && tid == 0) {
+        int a = 0;
+        for (int r = 0; r < kCC; ++r) a |= cflags[r];
+        *cd.nflags = a;
+    }
+    CHOL_PHASE(60);
+}
+
 // Deterministic pseudo-random candidate for completing a rank-deficient column.
 __device__ __forceinline__ float cand_value(int k, int attempt, int i) {
     const uint64_t h = splitmix64(0xC0FFEEULL ^ ((uint64_t)k << 40) ^ ((uint64_t)attempt << 32) ^ (uint64_t)i);
@@ -640,6 +1061,15 @@ __global__ void __launch_bounds__(256) fill_kernel(const CompleteDesc* __restric
 
 }  // namespace
 
+// RKFAC_CHOLINV_SINGLE=1 forces the single-CTA kernel (A/B checks and tools/chol_bench)
+static bool cholinv_single_cta() {
+    static const bool v = [] {
+        const char* e = getenv("RKFAC_CHOLINV_SINGLE");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 size_t cholinv_smem_bytes(int wmax, bool fp64) {
     const int es = fp64 ? 8 : 4;
     return (size_t)cholinv_state_bytes(wmax, es) + (size_t)prow(wmax) * es;
@@ -649,6 +1079,18 @@ void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, 
                     cudaStream_t s) {
     if (nfactors == 0) return;
     RKFAC_REQUIRE(wmax <= kMaxW, RKFAC_INVALID_ARGUMENT, "sketch width above 512 is not supported");
+    if (wmax > kNB && !cholinv_single_cta()) {
+        auto kc = fp64 ? (gram64 ? cholinv_cluster_kernel<double, double> : cholinv_cluster_kernel<float, double>)
+                       : (gram64 ? cholinv_cluster_kernel<double, float> : cholinv_cluster_kernel<float, float>);
+        const size_t cb = cc_smem_bytes(wmax, fp64 ? 8 : 4);
+        if (cb <= max_dynamic_smem((const void*)kc)) {
+            RKFAC_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb));
+            kc<<<nfactors * kCC, kCcThreads, cb, s>>>(d_descs, tol);
+            count_launch();
+            RKFAC_CHECK_LAUNCH();
+            return;
+        }
+    }
     const size_t bytes = cholinv_smem_bytes(wmax, fp64);
     auto ks = fp64 ? (gram64 ? cholinv_kernel<double, double, true> : cholinv_kernel<float, double, true>)
                    : (gram64 ? cholinv_kernel<double, float, true> : cholinv_kernel<float, float, true>);
