@@ -19,6 +19,7 @@
 #include <cmath>
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -351,6 +352,307 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kTcThreads)
             ed.evec[0] = 0.0;
             ed.tau[0] = 0.0;
         }
+    }
+    cluster.sync();  // no CTA leaves while others may still write into its shared memory
+}
+
+// --------------------------------------------------------- tridiag on a CTA cluster, one barrier per column
+// Same reduction, same cluster shape (CTA q owns the full rows i = q mod 4), restructured so that each column step
+// costs ONE cluster barrier and ONE pass over the owned rows:
+//   * every warp holds the reflector v_k, w_k and the next reflector v_{k+1} in registers, indexed by absolute
+//     column (lane + 32 t), and derives them redundantly: after the barrier of step k it has p_k (pushed by the row
+//     owners) and the entries of column k+1 as they were before update k (pushed one step early), so
+//     w_k = p_k - (tau_k/2)(p_k.v_k) v_k and column k+1 after update k, hence v_{k+1}, need no further exchange;
+//   * the pass over an owned row i applies update k (A_ij -= v_i w_j + w_i v_j, explicitly rounded products so
+//     that row j's owner and the redundant column computation agree bit for bit) and accumulates
+//     p_{k+1,i} = tau_{k+1} A_i. v_{k+1} from the updated values, then pushes (p_{k+1,i}, A_{i,k+2}) to every CTA
+//     as one 16-byte store (double-buffered by step parity: with one barrier per step no CTA is more than one
+//     step ahead of another).
+template <int NT>
+__device__ __forceinline__ double sel_slot(const double (&a)[NT], int s) {
+    double r = 0.0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) r = (t == s) ? a[t] : r;
+    return r;
+}
+// element j of a register vector held as v[t] at lane j % 32, slot j / 32 (uniform j across the warp)
+template <int NT>
+__device__ __forceinline__ double vget(const double (&a)[NT], int j) {
+    return __shfl_sync(0xffffffffu, sel_slot<NT>(a, j >> 5), j & 31);
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double rank2(double a, double vi, double wj, double wi, double vj) {
+    return __dsub_rn(a, __dadd_rn(__dmul_rn(vi, wj), __dmul_rn(wi, vj)));
+}
+
+#ifndef RKFAC_T1B_THREADS
+#define RKFAC_T1B_THREADS 256
+#endif
+#ifndef RKFAC_T1B_U
+#define RKFAC_T1B_U 1
+#endif
+#ifndef RKFAC_T1B_LOADFIRST
+#define RKFAC_T1B_LOADFIRST 1
+#endif
+constexpr int kT2Threads = RKFAC_T1B_THREADS;
+constexpr int kT2Warps = kT2Threads / 32;
+
+size_t tridiag1b_smem_bytes(int n) {
+    const int nloc = (n + kTcC - 1) / kTcC;
+    return ((((size_t)nloc * n + 1) & ~(size_t)1) + 4 * (size_t)n) * sizeof(double);
+}
+
+template <int NT, int U>
+__global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
+    tridiag1b_kernel(const EigDesc* __restrict__ descs) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int q = (int)cluster.block_rank();
+    const EigDesc& ed = descs[blockIdx.x / kTcC];
+    const int n = ed.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nloc = (n - q + kTcC - 1) / kTcC;  // rows i = q + 4 li
+    const bool writer = q == 0 && warp == 0;     // global outputs of the reflectors
+    extern __shared__ __align__(16) double tsm[];
+    double* R = tsm;                                                       // nloc x n
+    double2* pc = reinterpret_cast<double2*>(R + (((size_t)((n + kTcC - 1) / kTcC) * n + 1) & ~(size_t)1));
+    // pc: [2][n] of (p_i, A_{i,next column}), pushed by the row owners
+    auto push = [&](int buf, int i, double p, double c) {  // lanes 0..3 store into CTA `lane`
+        if (lane < kTcC) cluster.map_shared_rank(pc, lane)[buf * n + i] = make_double2(p, c);
+    };
+    for (int li = warp; li < nloc; li += kT2Warps) {
+        const int i = q + kTcC * li;
+        for (int j = lane; j < n; j += 32)
+            R[(size_t)li * n + j] =
+                0.5 * ((double)ed.A[(long long)i * ed.lda + j] + (double)ed.A[(long long)j * ed.lda + i]);
+    }
+    __syncthreads();
+    if (n < 3) {  // nothing to reduce
+        if (q == 0 && tid == 0) {
+            ed.dvec[0] = R[0];
+            ed.evec[0] = 0.0;
+            ed.tau[0] = 0.0;
+            if (n == 2) {
+                ed.evec[0] = R[1];
+                ed.tau[1] = 0.0;
+                ed.evec[1] = 0.0;
+            }
+        }
+        if (q == 1 && tid == 0 && n == 2) ed.dvec[1] = R[1];
+        return;
+    }
+    cluster.sync();  // every CTA runs: distributed shared memory may be written
+    // columns 0 and 1 (rows i >= 1) into buffer 1
+    for (int li = warp; li < nloc; li += kT2Warps) {
+        const int i = q + kTcC * li;
+        if (i >= 1) push(1, i, R[(size_t)li * n], R[(size_t)li * n + 1]);
+    }
+    if (q == 0 && tid == 0) ed.dvec[0] = R[0];
+    cluster_barrier();
+
+    // reflector from a column x (entries j >= b; x_b = alpha): v_b = 1, v_j = x_j / (alpha - beta)
+    double V[NT], W[NT], Vn[NT];
+    double tau = 0.0, taun = 0.0;
+    auto reflector = [&](const double (&x)[NT], int b, double (&v)[NT], double& t) {
+        double sig = 0.0;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            if (j > b && j < n) sig += x[s] * x[s];
+        }
+        sig = warp_sum_d(sig);
+        const double alpha = vget<NT>(x, b);
+        double beta = alpha;
+        t = 0.0;
+        if (sig > 0.0) {
+            const double nrm = sqrt(alpha * alpha + sig);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            t = (beta - alpha) / beta;
+        }
+        const double scale = (sig > 0.0) ? 1.0 / (alpha - beta) : 0.0;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            v[s] = (j == b) ? 1.0 : ((j > b && j < n) ? x[s] * scale : 0.0);
+        }
+        return beta;
+    };
+    auto write_refl = [&](int k, const double (&v)[NT], double beta, double t) {
+        if (!writer) return;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            if (j > k && j < n) ed.refl[(long long)k * n + (j - k - 1)] = v[s];
+        }
+        if (lane == 0) {
+            ed.evec[k] = beta;
+            ed.tau[k] = t;
+        }
+    };
+    {
+        double x[NT];
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            x[s] = (j >= 1 && j < n) ? pc[n + j].x : 0.0;
+        }
+        const double beta = reflector(x, 1, V, tau);
+        write_refl(0, V, beta, tau);
+    }
+    // p_0 over the owned rows i >= 1, with column 1 (rows >= 1) re-pushed alongside into buffer 0
+    for (int li = warp; li < nloc; li += kT2Warps) {
+        const int i = q + kTcC * li;
+        if (i < 1) continue;
+        const double* row = R + (size_t)li * n;
+        double dot = 0.0;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            if (j >= 1 && j < n) dot += row[j] * V[s];
+        }
+        dot = warp_sum_d(dot);
+        push(0, i, tau * dot, row[1]);
+    }
+    cluster_barrier();
+
+    for (int k = 0; k + 2 < n; ++k) {
+        const int b = k + 1;  // update k acts on indices >= b
+        const double2* cur = pc + (k & 1) * n;
+        TRC_PHASE(k, 8);
+        // w_k = p_k - (tau_k / 2)(p_k . v_k) v_k
+        double P[NT];
+        double pv = 0.0;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            P[s] = (j >= b && j < n) ? cur[j].x : 0.0;
+            pv += P[s] * V[s];
+        }
+        pv = warp_sum_d(pv);
+        const double alpha2 = -0.5 * tau * pv;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) W[s] = P[s] + alpha2 * V[s];
+        // column b+... : x = column b after update k (entries j >= b; j = b is the diagonal d_b)
+        const double vb = vget<NT>(V, b), wb = vget<NT>(W, b);
+        double x[NT];
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const int j = lane + 32 * s;
+            x[s] = (j >= b && j < n) ? rank2(cur[j].y, V[s], wb, W[s], vb) : 0.0;
+        }
+        const bool more = k + 3 < n;  // reflector b exists
+        if (writer) {
+            const double db = vget<NT>(x, b);
+            if (lane == 0) ed.dvec[b] = db;
+        }
+        if (more) {
+            const double beta = reflector(x, b + 1, Vn, taun);
+            write_refl(b, Vn, beta, taun);
+        } else {
+            // last 2 x 2: d_{n-1} comes from the pushed diagonal after this update; e_{n-2} = x_{n-1}
+            const double e = vget<NT>(x, n - 1);
+            if (writer && lane == 0) {
+                ed.evec[n - 2] = e;
+                ed.tau[n - 2] = 0.0;
+                ed.evec[n - 1] = 0.0;
+                ed.tau[n - 1] = 0.0;
+            }
+#pragma unroll
+            for (int s = 0; s < NT; ++s) Vn[s] = 0.0;
+            taun = 0.0;
+        }
+        TRC_PHASE(k, 9);
+        // one pass over the owned rows i >= b + 1: apply update k, accumulate p_{k+1,i}, push with A_{i,b+1};
+        // U rows of the warp at a time (independent chains overlap; the loop over row chunks stays rolled so the
+        // step's code fits the instruction cache)
+        {
+            const int li_first = max(0, (b + 1 - q + kTcC - 1) / kTcC);  // first owned row >= b + 1
+#pragma unroll 1
+            for (int l0 = li_first + warp; l0 < nloc; l0 += U * kT2Warps) {
+                double vi[U], wi[U], dot[U], cn[U];
+                double* row[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    ok[u] = l0 + u * kT2Warps < nloc;
+                    const int li = min(l0 + u * kT2Warps, nloc - 1);
+                    const int i = q + kTcC * li;
+                    vi[u] = vget<NT>(V, i);
+                    wi[u] = vget<NT>(W, i);
+                    dot[u] = 0.0;
+                    cn[u] = 0.0;
+                    row[u] = R + (size_t)li * n;
+                }
+#if RKFAC_T1B_LOADFIRST
+                // all loads first (stores to one row must not order the loads of another), then the updates,
+                // then the stores
+                double a[U][NT];
+#pragma unroll
+                for (int s = 0; s < NT; ++s) {
+                    const int j = lane + 32 * s;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) a[u][s] = (ok[u] && j >= b + 1 && j < n) ? row[u][j] : 0.0;
+                }
+#pragma unroll
+                for (int s = 0; s < NT; ++s) {
+                    const int j = lane + 32 * s;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        a[u][s] = rank2(a[u][s], vi[u], W[s], wi[u], V[s]);
+                        dot[u] += a[u][s] * Vn[s];  // Vn is zero outside [b + 1, n)
+                        if (j == b + 1) cn[u] = a[u][s];
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < NT; ++s) {
+                    const int j = lane + 32 * s;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (ok[u] && j >= b + 1 && j < n) row[u][j] = a[u][s];
+                }
+#else
+#pragma unroll
+                for (int s = 0; s < NT; ++s) {
+                    const int j = lane + 32 * s;
+                    if (j >= b + 1 && j < n) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (ok[u]) {
+                                const double a = rank2(row[u][j], vi[u], W[s], wi[u], V[s]);
+                                row[u][j] = a;
+                                dot[u] += a * Vn[s];
+                                if (j == b + 1) cn[u] = a;
+                            }
+                        }
+                    }
+                }
+#endif
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int li = l0 + u * kT2Warps;
+                    const double c = __shfl_sync(0xffffffffu, cn[u], (b + 1) & 31);
+                    if (li < nloc) push((k + 1) & 1, q + kTcC * li, taun * dot[u], c);
+                }
+            }
+        }
+        TRC_PHASE(k, 10);
+        cluster_barrier();
+        TRC_PHASE(k, 11);
+        if (!more) {
+            if (writer && lane == 0) ed.dvec[n - 1] = pc[((k + 1) & 1) * n + (n - 1)].y;
+            break;
+        }
+#pragma unroll
+        for (int s = 0; s < NT; ++s) V[s] = Vn[s];
+        tau = taun;
     }
     cluster.sync();  // no CTA leaves while others may still write into its shared memory
 }
@@ -983,8 +1285,17 @@ size_t tridiag_smem_bytes(int nmax) { return (size_t)nmax * (nmax + 1) / 2 * 8; 
 void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaStream_t s) {
     if (nfactors == 0) return;
     RKFAC_REQUIRE(nmax <= kMaxN, RKFAC_INVALID_ARGUMENT, "core size above 512 is not supported");
+    static const bool old_tridiag = [] {
+        const char* e = getenv("RKFAC_TRIDIAG_TWO_BARRIER");
+        return e && e[0] == '1';
+    }();
+    const size_t b1 = tridiag1b_smem_bytes(nmax);
+    auto k1 = nmax <= 256 ? tridiag1b_kernel<8, RKFAC_T1B_U> : tridiag1b_kernel<10, RKFAC_T1B_U>;
     const size_t cbytes = tridiag_cluster_smem_bytes(nmax);
-    if (nmax <= kTcMaxN && cbytes <= max_dynamic_smem((const void*)tridiag_cluster_kernel)) {
+    if (!old_tridiag && nmax <= 320 && b1 <= max_dynamic_smem((const void*)k1)) {
+        RKFAC_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b1));
+        k1<<<nfactors * kTcC, kT2Threads, b1, s>>>(d_descs);
+    } else if (nmax <= kTcMaxN && cbytes <= max_dynamic_smem((const void*)tridiag_cluster_kernel)) {
         RKFAC_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)cbytes));
         tridiag_cluster_kernel<<<nfactors * kTcC, kTcThreads, cbytes, s>>>(d_descs);

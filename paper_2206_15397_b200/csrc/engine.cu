@@ -2,8 +2,8 @@
 //
 // Data layout in HBM (per factor f, d = dim, w = r + p after clamping, rnla.hpp:35-43; dp = d rounded up to 32,
 // wp = w rounded up to 4 so every row pitch is a legal TMA stride):
-//   X_f        d x d FP32 EA factor (caller-owned, exactly symmetric) + its TF32 lo plane Xl (written by the EA
-//              epilogue, or by a split pass when the factor was changed outside a step)
+//   X_f        d x d FP32 EA factor (caller-owned, exactly symmetric); its TF32 lo plane is never stored: the
+//              X*Q products form it in shared memory from each TMA-loaded tile (tc_gemm.cu converter warps)
 //   S[0],S[1]  ping-pong sketch / basis roles, each in four planes: T = w x d (basis vectors contiguous: the
 //              K-major operand of X*Q, Y^T Y and Q^T Y), R = d x w (the K-major operand of Y L^-T), and the TF32
 //              lo planes of both (3xTF32 operands); every producer writes all four in its epilogue
@@ -58,7 +58,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
     if (const char* nf = std::getenv("RKFAC_FP64_ORTHS")) n_fp64_orth_ = std::atoi(nf);
     Carver c;
     struct Offs {
-        size_t S[2][4], Xc, Xl, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
+        size_t S[2][4], Xc, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
             scr, piv, z, Pt, Ptlo, scale, zflags, bracket, Uti, Utilo, Ui, Uilo;
     };
     std::vector<Offs> offs(n);
@@ -88,7 +88,6 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
             o.S[s][3] = c.take<float>(d * wp);
         }
         o.Xc = c.take<float>(d * dp);
-        o.Xl = c.take<float>(d * dp);
         o.G64 = c.take<double>(w * wp);
         o.G32 = c.take<float>(w * wp);
         o.L64 = c.take<double>(w * wp);
@@ -128,7 +127,7 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
             F.S[s].R = at<float>(arena_, o.S[s][2]);
             F.S[s].Rlo = at<float>(arena_, o.S[s][3]);
         }
-        F.Xc = at<float>(arena_, o.Xc); F.Xl = at<float>(arena_, o.Xl);
+        F.Xc = at<float>(arena_, o.Xc);
         F.G64 = at<double>(arena_, o.G64); F.G32 = at<float>(arena_, o.G32);
         F.Linv64 = at<double>(arena_, o.L64); F.Linv32 = at<float>(arena_, o.L32);
         F.Linv32lo = at<float>(arena_, o.L32lo);
@@ -271,11 +270,11 @@ void Plan::build_decomp_stages() {
     omega_total_ = off;
     upload(d_omega_, omega_);
     upload(d_split_omega_, so);
-    // X lo plane (and padded copy when X is not a TMA operand)
+    // padded copy of X when X itself is not a legal TMA operand
     std::vector<SplitDesc> sx;
     long long sx_off = 0;
     for (auto& F : f_) {
-        sx.push_back(SplitDesc{F.X, x_tma_ok_ ? nullptr : F.Xc, F.Xl, F.d, F.d, F.ldx, F.ldxa, sx_off});
+        sx.push_back(SplitDesc{F.X, F.Xc, nullptr, F.d, F.d, F.ldx, F.ldxa, sx_off});
         sx_off += (long long)F.d * F.d;
     }
     upload(d_split_x_, sx);
@@ -298,7 +297,7 @@ void Plan::build_decomp_stages() {
             {
                 TcProblemDesc p;
                 p.M = F.d; p.N = F.w; p.K = F.d;
-                p.A = Xop; p.A_lo = F.Xl; p.lda = F.ldxa;
+                p.A = Xop; p.A_lo = nullptr; p.lda = F.ldxa;  // X's lo plane is formed in shared memory
                 p.B = Q.T; p.B_lo = Q.Tlo; p.ldb = F.dp;
                 p.out0 = out_t(Y.T, F.dp); p.lo0 = out_t(Y.Tlo, F.dp);
                 p.out1 = out_r(Y.R, F.wp); p.lo1 = out_r(Y.Rlo, F.wp);
@@ -404,7 +403,6 @@ void Plan::build_ea_stage(double rho, double scale) {
             p.beta = (float)rho;
             p.Cin = F.X; p.ldcin = F.ldx; p.cin_t = 0;
             p.out0 = out_r(F.X, F.ldx);
-            p.lo0 = out_r(F.Xl, F.ldxa);
             ea_tc_stage_->add(p);
             sm.push_back(SplitDesc{F.M, nullptr, F.Ml, F.d, (int)F.n, F.ldm, F.ldm, off});
             off += (long long)F.d * F.n;
@@ -544,7 +542,8 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     for (auto& F : f_)
         RKFAC_REQUIRE(F.q == qmax, RKFAC_INVALID_ARGUMENT, "all factors of a plan share power_iters");
     mark(kDecompose, true);
-    if (!x_lo_fresh) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);
+    (void)x_lo_fresh;
+    if (!x_tma_ok_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);  // padded TMA copy of X
     launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
     launch_split(d_split_omega_.as<SplitDesc>(), n, omega_total_, s);
     int cur_q = 1;  // the basis lives in S[cur_q]

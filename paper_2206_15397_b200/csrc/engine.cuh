@@ -43,7 +43,6 @@ struct FactorState {
     // plan-owned workspace (carved from the arena)
     Role S[2];                           // ping-pong sketch / basis
     float* Xc = nullptr;                 // padded copy of X (only when X itself is not a valid TMA operand)
-    float* Xl = nullptr;                 // TF32 lo plane of X (pitch = ldxa)
     long long ldxa = 0;                  // pitch of the X operand actually fed to TMA (ldx or dp)
     float* Ml = nullptr;                 // TF32 lo plane of the samples (d x n, pitch ldm)
     double* G64 = nullptr;               // w x w

@@ -16,6 +16,9 @@
 //               K block; tcgen05.commit -> stage empty; after the last K block -> accumulator full
 //   warps 2..5  epilogue: tcgen05.ld 32x32b (TMEM lane = output row) -> fused alpha/scales/axpy -> up to four
 //               outputs in either layout (+ TF32 lo planes); split-K tiles store raw partials instead
+//   warps 6..7  lo-plane converters: for problems without a stored A lo plane (the EA factor X, read by every
+//               power product) the A_lo slot of each stage is formed in shared memory from the TMA-loaded A tile
+//               (x - tf32(x), same swizzled layout), so X's lo plane never travels through HBM
 // Two TMEM accumulators (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1.
 #include <cudaTypedefs.h>
 
@@ -46,11 +49,13 @@ struct StageCfg {
     static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTileBytes;
 };
 constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 4 * 48 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;
+constexpr int kConvThreads = 64;  // warps 6..7
 
 struct __align__(8) SmemBarriers {
     uint64_t full[kMaxStages];
     uint64_t empty[kMaxStages];
+    uint64_t conv[kMaxStages];  // A lo slot of the stage formed (converter warps)
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
     uint32_t tmem_base;
@@ -374,6 +379,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
+            mbar_init(&bars->conv[s], kConvThreads / 32);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->tmem_full[a], 1);
@@ -400,17 +406,18 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
                 const CUtensorMap* mp = maps + 4 * tl.prob;
-                const uint32_t bytes = (tl.pair ? 4u : 2u) * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
+                const uint32_t aplanes = pr.a_conv ? 1u : 2u;
+                const uint32_t bytes = (tl.pair ? 2u : 1u) * aplanes * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
                     unsigned char* st = smem + stage * kStageBytes;
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
                     tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
-                    tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    if (!pr.a_conv) tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
                     if (kPair && tl.pair) {
                         tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, tl.m0 + kBM);
-                        tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
+                        if (!pr.a_conv) tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
                     }
                     tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
                     tma_load_2d(st + 2 * kSub * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
@@ -438,6 +445,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const uint32_t idesc = idesc_tf32(pr.n_tile);
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
+                    mbar_wait(&bars->conv[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
                     const uint32_t b_hi = st + 2 * kSub * kATileBytes, b_lo = b_hi + kBTileBytes;
@@ -461,6 +469,35 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     ++uses[slot0 + sub];
                 }
                 if (!(kPair && tl.pair)) rr ^= 1;
+            }
+        }
+    } else if (warp >= 6) {
+        // ---------------- A lo-plane converters ----------------
+        const int ct = threadIdx.x - 6 * 32;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = t_begin; t < t_end; ++t) {
+            const TcTile tl = tiles[t];
+            const bool conv = probs[tl.prob].a_conv != 0;
+            const int nsub = (kPair && tl.pair) ? 2 : 1;
+            for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+                mbar_wait(&bars->full[stage], phase);  // also paces the arrivals of unconverted problems
+                if (conv) {
+                    unsigned char* st = smem + stage * kStageBytes;
+                    for (int sub = 0; sub < nsub; ++sub) {
+                        const float4* src = reinterpret_cast<const float4*>(st + sub * kATileBytes);
+                        float4* dst = reinterpret_cast<float4*>(st + (kSub + sub) * kATileBytes);
+#pragma unroll
+                        for (int i = 0; i < kATileBytes / 16 / kConvThreads; ++i) {
+                            const float4 x = src[i * kConvThreads + ct];
+                            dst[i * kConvThreads + ct] = lo4(x);
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->conv[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
     } else {
@@ -644,7 +681,7 @@ __global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long lo
         const int r = (int)(local / sd.cols), c = (int)(local - (long long)r * sd.cols);
         const float x = sd.src[(long long)r * sd.lds + c];
         if (sd.hi) sd.hi[(long long)r * sd.ldd + c] = x;
-        sd.lo[(long long)r * sd.ldd + c] = x - tf32_trunc(x);
+        if (sd.lo) sd.lo[(long long)r * sd.ldd + c] = x - tf32_trunc(x);
     }
 }
 
@@ -710,8 +747,9 @@ int TcGemm::add(const TcProblemDesc& d) {
     RKFAC_REQUIRE(!(d.sym && ks > 1), RKFAC_INVALID_ARGUMENT, "sym tc problem cannot be split");
     p.ksplit = ks;
     const int kper = (int)ceil_div(p.kblocks, ks);
+    p.a_conv = d.A_lo ? 0 : 1;
     maps_.push_back(make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
-    maps_.push_back(make_map(d.A_lo, d.K, d.M, d.lda, kBK, kBM));
+    maps_.push_back(make_map(d.A_lo ? d.A_lo : d.A, d.K, d.M, d.lda, kBK, kBM));
     maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, per));
     maps_.push_back(make_map(d.B_lo, d.K, d.N, d.ldb, kBK, per));
     for (int s = 0; s < ks; ++s) {

@@ -25,7 +25,7 @@ struct TcOut {
 
 struct TcProblemDesc {
     int M = 0, N = 0, K = 0;
-    const float* A = nullptr; const float* A_lo = nullptr; long long lda = 0;
+    const float* A = nullptr; const float* A_lo = nullptr; long long lda = 0;  // A_lo null: formed in smem
     const float* B = nullptr; const float* B_lo = nullptr; long long ldb = 0;
     float alpha = 1.f, beta = 0.f, gamma = 0.f;
     const float* rs = nullptr;
@@ -38,7 +38,7 @@ struct TcProblemDesc {
 };
 
 struct TcProb {  // device copy
-    int M, N, K, kblocks, ksplit, sym, n_tile, pad_;
+    int M, N, K, kblocks, ksplit, sym, n_tile, a_conv;  // a_conv: A lo plane formed in shared memory
     float alpha, beta, gamma, pad2_;
     const float* rs; const float* cs;
     const float* Cin; long long ldcin; int cin_t, din_t;
