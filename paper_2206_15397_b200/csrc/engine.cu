@@ -47,6 +47,16 @@ constexpr double kTol64 = 1e-13;  // relative pivot floor for rank deficiency, F
 constexpr double kTol32 = 1e-5;   // FP32 Gram (see cholqr.cu)
 
 TcOut out_t(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 1; return o; }
+// The tensor core's FP32 accumulation truncates: the error of one TMEM accumulation chain grows linearly with its
+// length (tools/tc_acc.cu, 3xTF32: 7.5e-6 at K = 1024, 2.9e-5 at K = 4096, 1.2e-4 at K = 16384).  The products
+// whose accuracy reaches the outputs -- the Gram matrices of the orthonormalisation, the final X*Q, the core
+// Q^T X Q and the two long-K products of the apply stage -- are split into K slices of at most kSliceK (partials
+// summed in FP32 by the deterministic split-K reduction).  The intermediate power products only carry a subspace
+// and stay unsplit.  Measured on d = 16384 (config 5) against an FP64 restatement: eigenvalue error 1.8e-4 ->
+// 1.4e-5, orthonormality 1.1e-4 -> 7.8e-6.
+constexpr int kSliceK = 512;
+constexpr int kSliceKFinal = 1024;
+
 TcOut out_r(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 0; return o; }
 
 }  // namespace
@@ -282,6 +292,7 @@ void Plan::build_decomp_stages() {
 
     for (int dir = 0; dir < 2; ++dir) {
         xq_[dir] = std::make_unique<TcGemm>();
+        xqf_[dir] = std::make_unique<TcGemm>();
         gram_[dir] = std::make_unique<TcGemm>();
         tri_[dir] = std::make_unique<TcGemm>();
         core_[dir] = std::make_unique<TcGemm>();
@@ -302,6 +313,8 @@ void Plan::build_decomp_stages() {
                 p.out0 = out_t(Y.T, F.dp); p.lo0 = out_t(Y.Tlo, F.dp);
                 p.out1 = out_r(Y.R, F.wp); p.lo1 = out_r(Y.Rlo, F.wp);
                 xq_[dir]->add(p);
+                p.slice_k = kSliceKFinal;
+                xqf_[dir]->add(p);
             }
             // FP32 CholeskyQR of Y into Q:  G = Y^T Y (A = B = Y^T), then Q = Y L^-T (A = Y, B = Linv)
             {
@@ -310,6 +323,7 @@ void Plan::build_decomp_stages() {
                 g.A = Y.T; g.A_lo = Y.Tlo; g.lda = F.dp;
                 g.B = Y.T; g.B_lo = Y.Tlo; g.ldb = F.dp;
                 g.out0 = out_r(F.G32, F.wp);
+                g.slice_k = kSliceK;
                 gram_[dir]->add(g);
                 TcProblemDesc t;
                 t.M = F.d; t.N = F.w; t.K = F.w;
@@ -331,6 +345,7 @@ void Plan::build_decomp_stages() {
                 cc.A = Aop.T; cc.A_lo = Aop.Tlo; cc.lda = F.dp;
                 cc.B = Y.T; cc.B_lo = Y.Tlo; cc.ldb = F.dp;
                 cc.out0 = out_r(F.core, F.w);
+                cc.slice_k = kSliceK;
                 core_[dir]->add(cc);
             }
             // lift: srevd U = Q P_r (rnla.hpp:101); rsvd U = Y P_r diag(1/s) (eig.hpp:260-266); both layouts of U
@@ -349,7 +364,7 @@ void Plan::build_decomp_stages() {
         }
         // complete_[dir] completes the output of orth(src = dir), i.e. role S[dir ^ 1]
         upload(d_complete_[dir], comp);
-        xq_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
+        xq_[dir]->finalize(); xqf_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
     std::vector<CopyDesc> cp;
@@ -446,6 +461,7 @@ void Plan::build_apply_stages(double lambda) {
         p0.B = A.Uti; p0.B_lo = A.Utilo; p0.ldb = A.dp;
         p0.cs = A.bracket;
         p0.out0 = out_r(L.W1, A.rp); p0.lo0 = out_r(L.W1lo, A.rp);
+        p0.slice_k = kSliceK;
         ap_[0]->add(p0);
         TcProblemDesc p1;
         p1.M = G.d; p1.N = A.d; p1.K = A.r;
@@ -460,6 +476,7 @@ void Plan::build_apply_stages(double lambda) {
         p2.B = L.Mt; p2.B_lo = L.Mtlo; p2.ldb = dGp;
         p2.rs = G.bracket;
         p2.out0 = out_t(L.W2t, G.rp); p2.lo0 = out_t(L.W2tlo, G.rp);
+        p2.slice_k = kSliceK;
         ap_[2]->add(p2);
         TcProblemDesc p3;
         p3.M = G.d; p3.N = A.d; p3.K = G.r;
@@ -573,7 +590,9 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
         launch_complete(d_complete_[cur_q ^ 1].as<CompleteDesc>(), n, s);
     }
     const int y = cur_q ^ 1;
-    timed_xq(y);
+    mark(kXQ, true);
+    xqf_[y]->launch(s);
+    mark(kXQ, false);
     mark(kEig, true);
     core_[y]->launch(s);
     launch_eig(d_eig_.as<EigDesc>(), n, wmax_, rmax_, s);

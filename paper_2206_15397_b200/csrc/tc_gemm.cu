@@ -743,6 +743,15 @@ int TcGemm::add(const TcProblemDesc& d) {
         ks = 1;
         // long-K problems with few output tiles: >= 8 CTAs per problem, >= 32 K blocks a slice
         while (mn_tiles * ks < 8 && p.kblocks / (2 * ks) >= 32) ks *= 2;
+        // accuracy: the tensor core's FP32 accumulation truncates, so the error of one TMEM accumulation chain
+        // grows linearly with its length (tools/tc_acc.cu: 3xTF32 rel. error 7.5e-6 at K = 1024, 2.9e-5 at 4096);
+        // slices of at most `slice_k` K are summed in FP32 on the CUDA cores by the split-K reduction
+        static const int env_slice = [] {
+            const char* e = std::getenv("RKFAC_TC_SLICE_K");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int slice_k = d.slice_k > 0 ? d.slice_k : env_slice;
+        if (slice_k > 0 && !d.sym) ks = std::max(ks, (int)ceil_div(p.kblocks, std::max(1, slice_k / kBK)));
     }
     RKFAC_REQUIRE(!(d.sym && ks > 1), RKFAC_INVALID_ARGUMENT, "sym tc problem cannot be split");
     p.ksplit = ks;

@@ -35,6 +35,7 @@ struct TcProblemDesc {
     TcOut out0, out1, lo0, lo1;
     int sym = 0;       // M == N: upper tiles only, mirrored stores (exactly symmetric result)
     int ksplit = 0;    // 0 = choose automatically
+    int slice_k = 0;   // > 0: split K so no TMEM accumulation chain is longer than slice_k (accuracy)
 };
 
 struct TcProb {  // device copy
