@@ -571,6 +571,8 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
         xq_[y]->launch(s);
         mark(kXQ, false);
     };
+    // Every product is orthonormalised, as in the reference: skipping alternate orthonormalisations (X X Q, same
+    // span) was measured to lose the tail of the spectrum in FP32 (eigenvalue errors ~0.9 at index r-1).
     for (int o = 0; o < north; ++o) {
         const int y = cur_q ^ 1;
         timed_xq(y);

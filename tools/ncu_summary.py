@@ -1,45 +1,51 @@
-"""Summarise an ncu --set full report (one kernel launch) into a small text block for profiles/.
+"""One-screen summary of an `ncu --set full` report (the numbers DESIGN.md and bench.py quote).
 
-    python tools/ncu_summary.py report.ncu-rep [title]
+    python tools/ncu_summary.py report.ncu-rep "title" > profiles/rNN_name.txt
 """
 import csv
-import io
 import subprocess
 import sys
 
-KEYS = [
-    ("gpu__time_duration.sum", "duration"),
-    ("dram__bytes_read.sum", "dram read"),
-    ("dram__bytes_write.sum", "dram write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput % of peak"),
-    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tensor (tc) pipe active % (per active SM)"),
-    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
-    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
-    ("launch__grid_size", "grid"),
-    ("launch__block_size", "block"),
-    ("launch__registers_per_thread", "registers/thread"),
-    ("smsp__inst_executed.sum", "warp instructions"),
+METRICS = [
+    ("duration", "gpu__time_duration.sum"),
+    ("dram read", "dram__bytes_read.sum"),
+    ("dram write", "dram__bytes_write.sum"),
+    ("dram throughput % of peak", "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("tensor (tc) pipe active % (per active SM)", "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("tcgen05 UTC issue % (per active SM)", "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("SM throughput %", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("issue slots busy %", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    ("L2 hit rate %", "lts__t_sector_hit_rate.pct"),
+    ("grid", "launch__grid_size"),
+    ("block", "launch__block_size"),
+    ("registers/thread", "launch__registers_per_thread"),
+    ("dynamic smem/block", "launch__shared_mem_per_block_dynamic"),
+    ("warp instructions", "smsp__inst_executed.sum"),
 ]
 
 
 def main():
-    rep = sys.argv[1]
-    title = sys.argv[2] if len(sys.argv) > 2 else rep
+    rep, title = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    print(f"== {title}")
-    print(f"kernel: {vals[hdr.index('Kernel Name')][:120]}")
-    for key, label in KEYS:
-        if key in hdr:
-            i = hdr.index(key)
-            print(f"  {label:45s} {vals[i]} {units[i]}")
-    stall = [(float(vals[i] or 0), h) for i, h in enumerate(hdr)
-             if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
-    stall.sort(reverse=True)
-    print("  top stall reasons (warps per issue): " + ", ".join(
-        f"{h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}={v:.2f}"
-        for v, h in stall[:5]))
+    rows = list(csv.reader(out.splitlines()))
+    head, units = rows[0], rows[1]
+    for r in rows[2:]:
+        idx = {h: i for i, h in enumerate(head)}
+        print(f"== {title}")
+        print(f"kernel: {r[idx['Kernel Name']]}" if "Kernel Name" in idx else "")
+        for label, m in METRICS:
+            if m in idx:
+                print(f"  {label:<45} {r[idx[m]]} {units[idx[m]]}")
+        stalls = []
+        for h, i in idx.items():
+            if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+                try:
+                    stalls.append((float(r[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in stalls) or 1.0
+        top = ", ".join(f"{n}={100 * v / tot:.1f}%" for v, n in sorted(stalls, reverse=True)[:6])
+        print(f"  top stall reasons (share of samples): {top}")
 
 
 if __name__ == "__main__":
