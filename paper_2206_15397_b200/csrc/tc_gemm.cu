@@ -39,17 +39,33 @@ constexpr int kMaxStages = 4;
 constexpr int kMaxBN = 256;
 constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB (one 128-row A sub-tile)
 constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
-// Two shared-memory configurations (same ~192 KB):
-//   single tiles: 4 stages of [A hi][A lo][B hi][B lo] = 48 KB
-//   paired tiles: 3 stages of [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo] = 64 KB (256 rows share the B tile)
-template <bool kPair>
+// Three shared-memory configurations of the same ~192 KB region:
+//   kCfg 0, single tiles: 4 stages of [A hi][A lo][B hi][B lo] = 48 KB
+//   kCfg 1, paired tiles: 3 stages of [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo] = 64 KB (256 rows share the B tile)
+//   kCfg 2, EA update (symmetric 128 x 128 tiles, axpy input Cin): 3 stages of 32 KB (B tile of 128 rows) and, in
+//           the space freed, per epilogue warp a ring of kCinRing 32 x 32 chunks (Cin prefetched by cp.async, the
+//           output written in place) and two mirror chunks, all dense 128-byte rows in the TMA SWIZZLE_128B layout:
+//           each output chunk and its transpose leave by TMA bulk-tensor stores, so the epilogue -- a pure HBM
+//           stream -- keeps several chunks in flight per warp with a handful of instructions per chunk
+constexpr int kCinRing = 3;
+template <int kCfg>
 struct StageCfg {
-    static constexpr int kSub = kPair ? 2 : 1;
-    static constexpr int kStages = kPair ? 3 : 4;
-    static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTileBytes;
+    static constexpr int kSub = kCfg == 1 ? 2 : 1;
+    static constexpr int kStages = kCfg == 0 ? 4 : 3;
+    static constexpr int kBTile = kCfg == 2 ? kBM * kBK * 4 : kBTileBytes;
+    static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTile;
 };
 constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 4 * 48 KB
+constexpr int kChunkBytes = 32 * 32 * 4;                                   // dense swizzled 32 x 32 chunk
+constexpr int kEaRingOff = 3 * StageCfg<2>::kStageBytes;                   // 96 KB
+constexpr int kEaMirOff = kEaRingOff + 4 * kCinRing * kChunkBytes;         // 144 KB
+static_assert(kEaMirOff + 4 * 2 * kChunkBytes <= kStagesBytesMax, "EA smem");
+// byte offset of element (row r, column c) of a dense 32 x 32 FP32 chunk in the SWIZZLE_128B layout
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+    return (uint32_t)(r * 128 + ((((c >> 2) ^ (r & 7)) & 7) << 4) + (c & 3) * 4);
+}
 constexpr int kThreads = 256;
+constexpr int kMapsPerProb = 5;  // A, A_lo, B, B_lo, out0 (SWIZZLE_128B 32 x 32 store boxes; EA configuration)
 constexpr int kConvThreads = 64;  // warps 6..7
 
 struct __align__(8) SmemBarriers {
@@ -97,6 +113,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
             "r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -358,14 +380,16 @@ __device__ __forceinline__ void chunk_store_pair(const float (&v)[32], float* ph
 }
 
 // ------------------------------------------------------------------------------------------------ kernel
-template <bool kPair>
+template <int kCfg>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__ maps,
                const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
     __shared__ TcProb s_pr[4];  // per epilogue warp
-    constexpr int kStages = StageCfg<kPair>::kStages;
-    constexpr int kStageBytes = StageCfg<kPair>::kStageBytes;
-    constexpr int kSub = StageCfg<kPair>::kSub;
+    constexpr bool kPair = kCfg == 1;
+    constexpr int kStages = StageCfg<kCfg>::kStages;
+    constexpr int kStageBytes = StageCfg<kCfg>::kStageBytes;
+    constexpr int kSub = StageCfg<kCfg>::kSub;
+    constexpr int kBTileS = StageCfg<kCfg>::kBTile;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                            ~uintptr_t(1023));
@@ -405,7 +429,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             for (int t = t_begin; t < t_end; ++t) {
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
-                const CUtensorMap* mp = maps + 4 * tl.prob;
+                const CUtensorMap* mp = maps + kMapsPerProb * tl.prob;
                 const uint32_t aplanes = pr.a_conv ? 1u : 2u;
                 const uint32_t bytes = (tl.pair ? 2u : 1u) * aplanes * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
@@ -420,7 +444,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         if (!pr.a_conv) tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
                     }
                     tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
-                    tma_load_2d(st + 2 * kSub * kATileBytes + kBTileBytes, mp + 3, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kSub * kATileBytes + kBTileS, mp + 3, &bars->full[stage], k0, tl.n0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -448,7 +472,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     mbar_wait(&bars->conv[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
-                    const uint32_t b_hi = st + 2 * kSub * kATileBytes, b_lo = b_hi + kBTileBytes;
+                    const uint32_t b_hi = st + 2 * kSub * kATileBytes, b_lo = b_hi + kBTileS;
                     for (int sub = 0; sub < nsub; ++sub) {
                         const uint32_t tmem_d = tmem_base + (slot0 + sub) * kMaxBN;
                         const uint32_t a_hi = st + sub * kATileBytes, a_lo = st + (kSub + sub) * kATileBytes;
@@ -505,6 +529,35 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         const int q = warp % 4;  // TMEM lane quadrant this warp may access
         int rr = 0;
         uint32_t uses[2] = {0u, 0u};
+        // kCfg 2: Cin chunks of this warp in (tile, chunk) order, prefetched by cp.async two chunks ahead into a
+        // ring of kCinRing swizzled slots (zero-filled past the matrix edge); the output chunk is written in place
+        unsigned char* ring = smem + kEaRingOff + (warp - 2) * kCinRing * kChunkBytes;
+        unsigned char* mir = smem + kEaMirOff + (warp - 2) * 2 * kChunkBytes;
+        int cin_t = t_begin, cin_c = 0;  // next chunk to prefetch
+        auto cin_issue = [&](int slot) {
+            if (cin_t < t_end) {
+                const TcTile ct = tiles[cin_t];
+                const TcProb& cp = probs[ct.prob];
+                const int mb = ct.m0 + q * 32, nb = ct.n0 + cin_c * 32;
+                const int cc = lane & 7, nl = min(cp.N, ct.n0 + cp.n_tile);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int rr_ = i * 4 + (lane >> 3), mm = mb + rr_, n = nb + cc * 4;
+                    const int valid = (mm < cp.M) ? max(0, min(4, nl - n)) : 0;
+                    const float* src = valid ? cp.Cin + (long long)mm * cp.ldcin + n : cp.Cin;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                     smem_u32(ring + slot * kChunkBytes + sw128(rr_, cc * 4))),
+                                 "l"(src), "r"(valid * 4));
+                }
+                if (++cin_c * 32 >= cp.n_tile) { cin_c = 0; ++cin_t; }
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        int chunk_no = 0;  // chunks consumed by this warp
+        if constexpr (kCfg == 2) {
+            cin_issue(0);
+            cin_issue(1);
+        }
         for (int t = t_begin; t < t_end; ++t) {
           const TcTile tl = tiles[t];
           const int nsub = (kPair && tl.pair) ? 2 : 1;
@@ -530,7 +583,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             const int nlim = min(pr.N, tl.n0 + pr.n_tile);
             float (*tile)[kTP] = stage_tiles[warp - 2];
             // prefetch the first Cin chunk (row-major axpy input, e.g. the EA factor) before the accumulator is ready
-            const bool pf = pr.beta != 0.f && pr.cin_t == 0 && pr.ksplit <= 1;
+            const bool pf = kCfg != 2 && pr.beta != 0.f && pr.cin_t == 0 && pr.ksplit <= 1;
             float4 pre[8];
             if (pf) rm_issue(pre, pr.Cin, pr.ldcin, mbase, tl.n0, pr.M, nlim, lane);
             mbar_wait(&bars->tmem_full[acc], acc_phase);
@@ -560,6 +613,52 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 if (pr.cs) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] *= (nbase + j < nlim) ? pr.cs[nbase + j] : 0.f;
+                }
+                if constexpr (kCfg == 2) {
+                    // every EA tile has a Cin (host-checked): chunk_no's slot is complete once at most one younger
+                    // group (the next chunk's) is pending
+                    const int slot = chunk_no % kCinRing;
+                    unsigned char* cs = ring + slot * kChunkBytes;
+                    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int j4 = 0; j4 < 32; j4 += 4) {
+                        float4* pc = reinterpret_cast<float4*>(cs + sw128(lane, j4));
+                        const float4 c4 = *pc;
+                        v[j4] = fmaf(pr.beta, c4.x, v[j4]);
+                        v[j4 + 1] = fmaf(pr.beta, c4.y, v[j4 + 1]);
+                        v[j4 + 2] = fmaf(pr.beta, c4.z, v[j4 + 2]);
+                        v[j4 + 3] = fmaf(pr.beta, c4.w, v[j4 + 3]);
+                        *pc = make_float4(v[j4], v[j4 + 1], v[j4 + 2], v[j4 + 3]);  // the output chunk, in place
+                    }
+                    const bool full_off = !(diag && nbase <= mbase + 31);  // strictly above the diagonal block
+                    unsigned char* ms = mir + (chunk_no & 1) * kChunkBytes;
+                    if (full_off) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) *reinterpret_cast<float*>(ms + sw128(j, lane)) = v[j];
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            const CUtensorMap* om = maps + kMapsPerProb * tl.prob + 4;
+                            tma_store_2d(om, cs, nbase, mbase);  // chunk (m, n)
+                            tma_store_2d(om, ms, mbase, nbase);  // mirror (n, m)
+                        }
+                    } else {
+                        __syncwarp();
+                        if (nbase == mbase)  // the 32 x 32 diagonal chunk: upper part + mirror, per element
+                            chunk_store(v, pr.o[0], pr.ldo[0], 0, false, mbase, nbase, pr.M, nlim, true, true,
+                                        tile, lane);
+                        // chunks below the diagonal block are the mirrors of chunks above it: nothing to store
+                    }
+                    if (lane == 0) {
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        // the previous chunk's stores have read their smem: its ring slot and mirror buffer are free
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    }
+                    __syncwarp();
+                    cin_issue((chunk_no + 2) % kCinRing);
+                    ++chunk_no;
+                    continue;
                 }
                 if (pr.beta != 0.f) {
                     float cv[32];
@@ -599,6 +698,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             mbar_arrive(&bars->tmem_empty[acc]);
           }
         }
+        if (kCfg == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     if (warp == 1) {
@@ -698,7 +798,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-CUtensorMap make_map(const float* base, int inner, int outer, long long ld_elems, int box_inner, int box_outer) {
+CUtensorMap make_map(const float* base, int inner, int outer, long long ld_elems, int box_inner, int box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
     RKFAC_REQUIRE(base && (ld_elems * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0,
                   RKFAC_INVALID_ARGUMENT, "TMA operand needs a 16-byte aligned base and row pitch");
     CUtensorMap m;
@@ -707,7 +808,7 @@ CUtensorMap make_map(const float* base, int inner, int outer, long long ld_elems
     cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RKFAC_REQUIRE(r == CUDA_SUCCESS, RKFAC_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
     return m;
@@ -761,6 +862,9 @@ int TcGemm::add(const TcProblemDesc& d) {
     maps_.push_back(make_map(d.A_lo ? d.A_lo : d.A, d.K, d.M, d.lda, kBK, kBM));
     maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, per));
     maps_.push_back(make_map(d.B_lo, d.K, d.N, d.ldb, kBK, per));
+    const bool out_tma = d.out0.p && d.out0.t == 0 && tc_operand_ok(d.out0.p, d.out0.ld);
+    maps_.push_back(out_tma ? make_map(d.out0.p, d.N, d.M, d.out0.ld, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+                            : make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
     for (int s = 0; s < ks; ++s) {
         const int kb0 = s * kper, kb1 = std::min(p.kblocks, kb0 + kper);
         if (kb0 >= kb1) continue;
@@ -801,8 +905,14 @@ void TcGemm::finalize() {
             tiles_.swap(split);
         }
         // the 3 x 64 KB configuration also measured faster for the symmetric EA update (0.62 vs 0.84 ms, VGG16)
-        paired_ = false;
-        for (const auto& t : tiles_) paired_ = paired_ || t.pair || probs_[t.prob].sym;
+        bool paired = false, ea = !tiles_.empty();
+        for (const auto& t : tiles_) paired = paired || t.pair || probs_[t.prob].sym;
+        for (const auto& p : probs_)  // the EA configuration: symmetric axpy problems with an aligned row-major Cin
+            ea = ea && p.sym && p.beta != 0.f && p.cin_t == 0 && p.ksplit <= 1 && p.n_tile == kBM && p.Cin &&
+                 (p.ldcin % 4) == 0 && (reinterpret_cast<uintptr_t>(p.Cin) % 16) == 0 && p.o[0] && p.to[0] == 0 &&
+                 (p.ldo[0] % 4) == 0 && (reinterpret_cast<uintptr_t>(p.o[0]) % 16) == 0 && !p.o[1] && !p.o[2] &&
+                 !p.o[3] && !p.rs && !p.cs && p.gamma == 0.f;
+        cfg_ = ea ? 2 : (paired ? 1 : 0);
     }
     // split-K partial buffers
     size_t total = 0;
@@ -868,7 +978,7 @@ size_t TcGemm::smem_bytes() { return (size_t)kStagesBytesMax + kBarrierBytes + k
 void TcGemm::launch(cudaStream_t s) const {
     if (tiles_.empty()) return;
     const size_t smem = smem_bytes();
-    auto k = paired_ ? tc_gemm_kernel<true> : tc_gemm_kernel<false>;
+    auto k = cfg_ == 2 ? tc_gemm_kernel<2> : (cfg_ == 1 ? tc_gemm_kernel<1> : tc_gemm_kernel<0>);
     RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(), d_tiles_.as<TcTile>(),
                                      d_begin_.as<int>());

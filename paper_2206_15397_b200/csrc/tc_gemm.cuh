@@ -73,7 +73,7 @@ class TcGemm {
     std::vector<size_t> partial_off_;
     int nctas_ = 0;
     bool any_split_ = false;
-    bool paired_ = false;  // launch the paired-tile (3 x 64 KB stage) kernel
+    int cfg_ = 0;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
     int nred_ = 0;
     long long red_total_ = 0;
     DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_, d_red_;
