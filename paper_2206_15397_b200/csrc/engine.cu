@@ -255,7 +255,7 @@ void Plan::bind_layers(int nl, const int* a, const int* g, const float* const* J
         L.W2t = at<float>(layer_arena_, o[l][6]); L.W2tlo = at<float>(layer_arena_, o[l][7]);
         const FactorState &A = f_[L.a], &G = f_[L.g];
         const long long dAp = (A.d + 3) / 4 * 4;
-        sj.push_back(SplitDesc{L.J, L.Jc, L.Jlo, G.d, A.d, A.d, dAp, off});
+        sj.push_back(SplitDesc{L.J, L.Jc, nullptr, G.d, A.d, A.d, dAp, off});  // aligned copy (lo formed in smem)
         off += (long long)G.d * A.d;
     }
     upload(d_split_j_, sj);
@@ -265,7 +265,7 @@ void Plan::bind_layers(int nl, const int* a, const int* g, const float* const* J
 
 void Plan::build_decomp_stages() {
     const int n = nfactors();
-    // Omega^T written into S[1].T (the initial basis role), its lo plane by a split pass.
+    // Omega^T written into S[1].T (the initial basis role) together with its TF32 lo plane.
     omega_.resize(n);
     long long off = 0;
     std::vector<SplitDesc> so;
@@ -273,6 +273,7 @@ void Plan::build_decomp_stages() {
         FactorState& F = f_[i];
         OmegaDesc o{};
         o.d = F.d; o.w = F.w; o.ld = F.dp; o.out = F.S[1].T; o.tag = F.tag; o.seed = 0; o.ctr0 = 0; o.offset = off;
+        o.out_lo = F.S[1].Tlo;
         so.push_back(SplitDesc{F.S[1].T, nullptr, F.S[1].Tlo, F.w, F.d, F.dp, F.dp, off});
         off += (long long)F.d * F.w;
         omega_[i] = o;
@@ -315,6 +316,7 @@ void Plan::build_decomp_stages() {
                 xq_[dir]->add(p);
                 p.slice_k = kSliceKFinal;
                 xqf_[dir]->add(p);
+
             }
             // FP32 CholeskyQR of Y into Q:  G = Y^T Y (A = B = Y^T), then Q = Y L^-T (A = Y, B = Linv)
             {
@@ -411,8 +413,8 @@ void Plan::build_ea_stage(double rho, double scale) {
             if (!F.M || F.n == 0) continue;
             TcProblemDesc p;
             p.M = F.d; p.N = F.d; p.K = (int)F.n;
-            p.A = F.M; p.A_lo = F.Ml; p.lda = F.ldm;
-            p.B = F.M; p.B_lo = F.Ml; p.ldb = F.ldm;
+            p.A = F.M; p.A_lo = nullptr; p.lda = F.ldm;  // both lo planes of the samples formed in smem
+            p.B = F.M; p.B_lo = nullptr; p.ldb = F.ldm;
             p.sym = 1;
             p.alpha = (float)((1.0 - rho) * scale * scale);
             p.beta = (float)rho;
@@ -457,7 +459,7 @@ void Plan::build_apply_stages(double lambda) {
         const long long dAp = (A.d + 3) / 4 * 4, dGp = (G.d + 3) / 4 * 4;
         TcProblemDesc p0;
         p0.M = G.d; p0.N = A.r; p0.K = A.d;
-        p0.A = L.Jc; p0.A_lo = L.Jlo; p0.lda = dAp;
+        p0.A = L.Jc; p0.A_lo = nullptr; p0.lda = dAp;
         p0.B = A.Uti; p0.B_lo = A.Utilo; p0.ldb = A.dp;
         p0.cs = A.bracket;
         p0.out0 = out_r(L.W1, A.rp); p0.lo0 = out_r(L.W1lo, A.rp);
@@ -541,7 +543,6 @@ void Plan::ea_update(double rho, double scale) {
     cudaStream_t s = ctx_->stream;
     mark(kEA, true);
     if (ea_tc_) {
-        launch_split(d_split_m_.as<SplitDesc>(), nfactors(), split_m_total_, s);
         ea_tc_stage_->launch(s);
     } else {
         ea_simt_->launch(s);
@@ -562,11 +563,13 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     (void)x_lo_fresh;
     if (!x_tma_ok_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);  // padded TMA copy of X
     launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
-    launch_split(d_split_omega_.as<SplitDesc>(), n, omega_total_, s);
     int cur_q = 1;  // the basis lives in S[cur_q]
     const int north = 2 * qmax + 1;
     bool last_fp64 = false;
-    auto timed_xq = [&](int y) {
+    // Every power product runs in 3xTF32: 1xTF32 intermediate products (0.7 ms faster per VGG16 step) were measured
+    // to move the poorly converged Ritz values near the cut-off by up to 6e-3 (d = 16384) -- first order in the
+    // perturbation of the subspace -- so the reference's randomized answer is not reproduced to 1e-4.
+    auto timed_xq = [&](int y, int) {
         mark(kXQ, true);
         xq_[y]->launch(s);
         mark(kXQ, false);
@@ -575,7 +578,7 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     // span) was measured to lose the tail of the spectrum in FP32 (eigenvalue errors ~0.9 at index r-1).
     for (int o = 0; o < north; ++o) {
         const int y = cur_q ^ 1;
-        timed_xq(y);
+        timed_xq(y, o);
         last_fp64 = o < n_fp64_orth_;
         mark(kOrth, true);
         orth(y, last_fp64, s);  // S[y] -> S[cur_q]
@@ -614,7 +617,7 @@ void Plan::precondition(double lambda) {
     cudaStream_t s = ctx_->stream;
     mark(kApply, true);
     launch_bracket(d_bracket_.as<BracketDesc>(), nfactors(), lambda, s);
-    launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, s);  // J -> aligned copy + lo
+    launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, s);  // J -> aligned TMA copy
     for (auto& a : ap_) a->launch(s);
     mark(kApply, false);
 }

@@ -16,6 +16,7 @@ struct OmegaDesc {
     uint64_t ctr0;
     long long offset;   // prefix of d*w over factors
     int rowmajor;       // 1: out[i*ld + j] (rng.hpp layout, used by rkfac_sample_gaussian)
+    float* out_lo;      // optional TF32 lo plane (same layout): the 3xTF32 operand of the first X*Omega
 };
 // mode 0: seed_f = desc.seed; mode 1: seed_f = substream(root, step, tag_f)
 void launch_omega(const OmegaDesc* d_descs, int nfactors, long long total, int mode, uint64_t root, uint64_t step,

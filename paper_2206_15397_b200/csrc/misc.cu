@@ -35,7 +35,9 @@ __global__ void omega_kernel(const OmegaDesc* __restrict__ descs, int n, long lo
         const uint64_t seed = mode ? substream(root, step, od.tag) : od.seed;
         const uint64_t ctr = od.ctr0 + 2ULL * ((uint64_t)i * (uint64_t)od.w + (uint64_t)j);
         const float g = (float)gaussian_at(seed, ctr);
-        if (od.rowmajor) od.out[(long long)i * od.ld + j] = g; else od.out[(long long)j * od.ld + i] = g;
+        const long long o = od.rowmajor ? (long long)i * od.ld + j : (long long)j * od.ld + i;
+        od.out[o] = g;
+        if (od.out_lo) od.out_lo[o] = g - __uint_as_float(__float_as_uint(g) & 0xFFFFE000u);
     }
 }
 

@@ -430,21 +430,24 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const TcTile tl = tiles[t];
                 const TcProb& pr = probs[tl.prob];
                 const CUtensorMap* mp = maps + kMapsPerProb * tl.prob;
-                const uint32_t aplanes = pr.a_conv ? 1u : 2u;
-                const uint32_t bytes = (tl.pair ? 2u : 1u) * aplanes * kATileBytes + 2u * (uint32_t)pr.n_tile * kBK * 4u;
+                const uint32_t aplanes = (pr.a_conv || pr.single) ? 1u : 2u, bplanes = (pr.b_conv || pr.single) ? 1u : 2u;
+                const uint32_t bytes =
+                    (tl.pair ? 2u : 1u) * aplanes * kATileBytes + bplanes * (uint32_t)pr.n_tile * kBK * 4u;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
                     unsigned char* st = smem + stage * kStageBytes;
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
                     tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
-                    if (!pr.a_conv) tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    if (!pr.a_conv && !pr.single) tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
                     if (kPair && tl.pair) {
                         tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, tl.m0 + kBM);
-                        if (!pr.a_conv) tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
+                        if (!pr.a_conv && !pr.single)
+                            tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
                     }
                     tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
-                    tma_load_2d(st + 2 * kSub * kATileBytes + kBTileS, mp + 3, &bars->full[stage], k0, tl.n0);
+                    if (!pr.b_conv && !pr.single)
+                        tma_load_2d(st + 2 * kSub * kATileBytes + kBTileS, mp + 3, &bars->full[stage], k0, tl.n0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -467,6 +470,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 }
                 tc_fence_after();
                 const uint32_t idesc = idesc_tf32(pr.n_tile);
+                const bool single = pr.single != 0;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
                     mbar_wait(&bars->conv[stage], phase);
@@ -480,9 +484,12 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
                             const uint32_t first = (kb == tl.kb0 && kk == 0) ? 0u : 1u;
-                            mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
-                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
-                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc, 1u);
+                            if (!single) {
+                                mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
+                                mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
+                            }
+                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc,
+                                     single ? first : 1u);
                         }
                     }
                     mma_commit(&bars->empty[stage]);
@@ -502,7 +509,9 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         uint32_t phase = 0;
         for (int t = t_begin; t < t_end; ++t) {
             const TcTile tl = tiles[t];
-            const bool conv = probs[tl.prob].a_conv != 0;
+            const bool single = probs[tl.prob].single != 0;
+            const bool conv = probs[tl.prob].a_conv != 0 && !single, bconv = probs[tl.prob].b_conv != 0 && !single;
+            const int nb16 = probs[tl.prob].n_tile * kBK / 4;  // float4s of the B tile
             const int nsub = (kPair && tl.pair) ? 2 : 1;
             for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                 mbar_wait(&bars->full[stage], phase);  // also paces the arrivals of unconverted problems
@@ -517,8 +526,14 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                             dst[i * kConvThreads + ct] = lo4(x);
                         }
                     }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
                 }
+                if (bconv) {
+                    unsigned char* st = smem + stage * kStageBytes;
+                    const float4* src = reinterpret_cast<const float4*>(st + 2 * kSub * kATileBytes);
+                    float4* dst = reinterpret_cast<float4*>(st + 2 * kSub * kATileBytes + kBTileS);
+                    for (int i = ct; i < nb16; i += kConvThreads) dst[i] = lo4(src[i]);
+                }
+                if (conv || bconv) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tensor core
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->conv[stage]);
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -858,10 +873,12 @@ int TcGemm::add(const TcProblemDesc& d) {
     p.ksplit = ks;
     const int kper = (int)ceil_div(p.kblocks, ks);
     p.a_conv = d.A_lo ? 0 : 1;
+    p.b_conv = d.B_lo ? 0 : 1;
+    p.single = d.single;
     maps_.push_back(make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
     maps_.push_back(make_map(d.A_lo ? d.A_lo : d.A, d.K, d.M, d.lda, kBK, kBM));
     maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, per));
-    maps_.push_back(make_map(d.B_lo, d.K, d.N, d.ldb, kBK, per));
+    maps_.push_back(make_map(d.B_lo ? d.B_lo : d.B, d.K, d.N, d.ldb, kBK, per));
     const bool out_tma = d.out0.p && d.out0.t == 0 && tc_operand_ok(d.out0.p, d.out0.ld);
     maps_.push_back(out_tma ? make_map(d.out0.p, d.N, d.M, d.out0.ld, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
                             : make_map(d.A, d.K, d.M, d.lda, kBK, kBM));

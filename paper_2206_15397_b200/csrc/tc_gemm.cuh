@@ -26,7 +26,7 @@ struct TcOut {
 struct TcProblemDesc {
     int M = 0, N = 0, K = 0;
     const float* A = nullptr; const float* A_lo = nullptr; long long lda = 0;  // A_lo null: formed in smem
-    const float* B = nullptr; const float* B_lo = nullptr; long long ldb = 0;
+    const float* B = nullptr; const float* B_lo = nullptr; long long ldb = 0;  // B_lo null: formed in smem
     float alpha = 1.f, beta = 0.f, gamma = 0.f;
     const float* rs = nullptr;
     const float* cs = nullptr;
@@ -36,11 +36,14 @@ struct TcProblemDesc {
     int sym = 0;       // M == N: upper tiles only, mirrored stores (exactly symmetric result)
     int ksplit = 0;    // 0 = choose automatically
     int slice_k = 0;   // > 0: split K so no TMEM accumulation chain is longer than slice_k (accuracy)
+    int single = 0;    // 1: one TF32 MMA per product (no lo terms) -- for products that only carry a subspace
 };
 
 struct TcProb {  // device copy
     int M, N, K, kblocks, ksplit, sym, n_tile, a_conv;  // a_conv: A lo plane formed in shared memory
-    float alpha, beta, gamma, pad2_;
+    float alpha, beta, gamma;
+    int b_conv;  // B lo plane formed in shared memory
+    int single, pad3_;
     const float* rs; const float* cs;
     const float* Cin; long long ldcin; int cin_t, din_t;
     const float* Din; long long lddin;
