@@ -138,6 +138,9 @@ int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t rng_ro
  * and 7 counts indexed: 0 EA update, 1 decomposition, 2 preconditioning, 3 X*Q products (the GEMM stage),
  * 4 orthonormalisations, 5 core + eigensolve + lift, 6 whole step. */
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
+/* Cap the persistent tensor-core grids of this plan at `ctas` CTAs (0: one per SM), leaving SMs to the
+ * latency-bound per-factor kernels of plans running concurrently on other streams (StreamedStep). */
+int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas);
 int rkfac_plan_timing(rkfac_plan_t plan, float* sums_ms7, int* counts7);
 
 #ifdef __cplusplus

@@ -112,6 +112,7 @@ SIGNATURES = {
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "rkfac_plan_set_timing": (C.c_int, [_vp, C.c_int]),
+    "rkfac_plan_set_max_ctas": (C.c_int, [_vp, C.c_int]),
 }
 
 
@@ -378,6 +379,7 @@ class BatchedStep:
     n_samples: Sequence[int] = ()
     device: int = 0
     factor_indices: Optional[Sequence[int]] = None  # global factor tags (multi-GPU shards keep global seeds)
+    max_ctas: int = 0  # cap of the persistent tensor-core grids (0: all SMs; StreamedStep leaves SMs to other groups)
     factors: list = field(default_factory=list, init=False)
     bases_t: list = field(default_factory=list, init=False)
     dvals: list = field(default_factory=list, init=False)
@@ -400,6 +402,8 @@ class BatchedStep:
         meth = 1 if self.method == DecompMethod.SREVD else 0
         _check(lib.rkfac_plan_create(self.ctx.h, descs, len(dims), meth, C.byref(h)), self.ctx.h, "plan_create")
         self.h = h
+        if self.max_ctas:
+            _check(lib.rkfac_plan_set_max_ctas(h, int(self.max_ctas)), self.ctx.h, "set_max_ctas")
         dev = torch.device("cuda", self.device)
         self.ranks = [int(lib.rkfac_plan_rank(h, f)) for f in range(len(dims))]
         lds = []
@@ -482,6 +486,9 @@ class BatchedStep:
             pass
 
 
+STREAMED_TC_CTAS = 132
+
+
 class StreamedStep:
     """The batched step split into ``groups`` independent layer groups, each a :class:`BatchedStep` (its own plan)
     run on its own CUDA stream and joined back into the caller's stream.
@@ -495,7 +502,7 @@ class StreamedStep:
 
     def __init__(self, layers: Sequence[LayerSpec], groups: int = 2, rank: int = 220, oversampling: int = 10,
                  power_iters: int = 4, method: DecompMethod = DecompMethod.SREVD, n_samples: Sequence[int] = (),
-                 device: int = 0, factor_indices: Optional[Sequence[int]] = None):
+                 device: int = 0, factor_indices: Optional[Sequence[int]] = None, max_ctas: Optional[int] = None):
         from .partition import layer_cost, lpt_partition
 
         torch = _torch()
@@ -506,13 +513,18 @@ class StreamedStep:
         tags = list(factor_indices) if factor_indices is not None else list(range(2 * nl))
         costs = [layer_cost(L.dim_a, L.dim_g, rank, oversampling) for L in self.layers]
         self.parts = [p for p in lpt_partition(costs, max(1, min(groups, nl))) if p]
+        if max_ctas is None:
+            # a persistent tensor-core grid on every SM would keep the other groups' latency-bound kernels (Cholesky-
+            # inverse, tridiagonalisation clusters) waiting; 132 of 148 measured best for 2 VGG16 groups
+            max_ctas = STREAMED_TC_CTAS if len(self.parts) > 1 else 0
         ns = list(n_samples)
         self.subs = []
         for part in self.parts:
             sub_ns = ns if len(ns) <= 1 else [ns[2 * l + w] for l in part for w in (0, 1)]
             self.subs.append(BatchedStep([self.layers[l] for l in part], rank=rank, oversampling=oversampling,
                                          power_iters=power_iters, method=method, n_samples=sub_ns, device=device,
-                                         factor_indices=[tags[2 * l + w] for l in part for w in (0, 1)]))
+                                         factor_indices=[tags[2 * l + w] for l in part for w in (0, 1)],
+                                         max_ctas=max_ctas))
         self.ctx = self.subs[0].ctx
         self.streams = [torch.cuda.Stream(device=device) for _ in self.subs]
         # views in the original order

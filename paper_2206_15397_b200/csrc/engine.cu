@@ -292,14 +292,14 @@ void Plan::build_decomp_stages() {
     split_x_total_ = sx_off;
 
     for (int dir = 0; dir < 2; ++dir) {
-        xq_[dir] = std::make_unique<TcGemm>();
-        xqf_[dir] = std::make_unique<TcGemm>();
-        gram_[dir] = std::make_unique<TcGemm>();
-        tri_[dir] = std::make_unique<TcGemm>();
-        core_[dir] = std::make_unique<TcGemm>();
+        xq_[dir] = new_tc();
+        xqf_[dir] = new_tc();
+        gram_[dir] = new_tc();
+        tri_[dir] = new_tc();
+        core_[dir] = new_tc();
         gram64_[dir] = std::make_unique<Gram64Batch>();
         tri64_[dir] = std::make_unique<Tri64Batch>();
-        lift_[dir] = std::make_unique<TcGemm>();
+        lift_[dir] = new_tc();
         std::vector<CompleteDesc> comp;
         for (auto& F : f_) {
             Role& Y = F.S[dir];      // written by xq_[dir]; source of the orthonormalisation indexed dir
@@ -402,13 +402,26 @@ void Plan::build_decomp_stages() {
     upload(d_bracket_, br);
 }
 
+std::unique_ptr<TcGemm> Plan::new_tc() const {
+    auto g = std::make_unique<TcGemm>();
+    g->set_max_ctas(tc_cap_);
+    return g;
+}
+
+void Plan::set_max_ctas(int n) {
+    tc_cap_ = n;
+    if (factors_bound_) build_decomp_stages();
+    ea_rho_ = -1;  // EA and apply stages are rebuilt on their next use
+    ap_lambda_ = -1;
+}
+
 void Plan::build_ea_stage(double rho, double scale) {
     ea_tc_stage_.reset();
     ea_simt_.reset();
     std::vector<SplitDesc> sm;
     long long off = 0;
     if (ea_tc_) {
-        ea_tc_stage_ = std::make_unique<TcGemm>();
+        ea_tc_stage_ = new_tc();
         for (auto& F : f_) {
             if (!F.M || F.n == 0) continue;
             TcProblemDesc p;
@@ -452,7 +465,7 @@ void Plan::build_apply_stages(double lambda) {
     //                                 mid^T = (W1 U_A^T + J/lambda)^T (M=dG, N=dA, K=rA)
     //   LEFT  (kfactor.hpp:147-152):  W2^T = (diag(b_G) U_G^T mid)^T  (M=rG, N=dA, K=dG)
     //                                 out = U_G W2 + mid/lambda        (M=dG, N=dA, K=rG)
-    for (auto& a : ap_) a = std::make_unique<TcGemm>();
+    for (auto& a : ap_) a = new_tc();
     const float inv = (float)(1.0 / lambda);
     for (auto& L : layers_) {
         const FactorState &A = f_[L.a], &G = f_[L.g];

@@ -103,6 +103,7 @@ class Plan {
 
     enum TimingKind { kEA = 0, kDecompose = 1, kApply = 2, kXQ = 3, kOrth = 4, kEig = 5, kStep = 6, kTimingKinds = 7 };
     void set_timing(bool on) { timing_ = on; timing_reset(); }
+    void set_max_ctas(int n);
     void timing_reset();
     // Sums (ms) and counts of each timed region since the last reset; call after the stream is synchronised.
     void timing_report(float* sums, int* counts) const;
@@ -114,6 +115,7 @@ class Plan {
 
   private:
     void build_decomp_stages();
+    std::unique_ptr<TcGemm> new_tc() const;
     void build_ea_stage(double rho, double scale);
     void build_apply_stages(double lambda);
     void orth(int src, bool fp64, cudaStream_t s);
@@ -147,6 +149,7 @@ class Plan {
     // ill-conditioned enough (kappa ~1e4) to break FP32 CholeskyQR; measured on B200: 1 vs 2 FP64
     // orths give the same parity error, 0 gives eigenvalue errors of ~5e-2.
     int n_fp64_orth_ = 1;
+    int tc_cap_ = 0;  // persistent tensor-core grid cap (0: all SMs)
 
     bool timing_ = false;
     struct Rec { int kind; size_t b, e; };

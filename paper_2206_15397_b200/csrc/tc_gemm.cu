@@ -954,7 +954,7 @@ void TcGemm::finalize() {
     nred_ = (int)red.size();
     // LPT over persistent CTAs: tile cost ~ K blocks * (n_tile + epilogue overhead)
     const int ntiles = (int)tiles_.size();
-    int cap = kNumSMs;
+    int cap = cap_ > 0 ? std::min(kNumSMs, cap_) : kNumSMs;
     if (const char* e = std::getenv("RKFAC_TC_MAX_CTAS")) cap = std::max(1, std::min(kNumSMs, std::atoi(e)));
     nctas_ = std::max(1, std::min(ntiles, cap));
     std::vector<int> order(ntiles);

@@ -63,6 +63,7 @@ struct TcRed {  // split-K reduction map: first 32x32 output tile of a split pro
 class TcGemm {
   public:
     int add(const TcProblemDesc& d);
+    void set_max_ctas(int n) { cap_ = n; }  // persistent-grid cap (0: all SMs); leaves SMs to concurrent streams
     void finalize();
     void launch(cudaStream_t s) const;
     bool empty() const { return tiles_.empty(); }
@@ -76,7 +77,8 @@ class TcGemm {
     std::vector<size_t> partial_off_;
     int nctas_ = 0;
     bool any_split_ = false;
-    int cfg_ = 0;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
+    int cfg_ = 0;
+    int cap_ = 0;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
     int nred_ = 0;
     long long red_total_ = 0;
     DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_, d_red_;
