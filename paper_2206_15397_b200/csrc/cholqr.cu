@@ -66,6 +66,22 @@ __host__ __device__ __forceinline__ int cholinv_state_bytes(int n, int es) {
     return (es * (kNB * (kNB + 1) + kNB) + 4 * rup4(n) + rup4(n) + 15) & ~15;
 }
 
+// G(i, j) (the element itself: the Gram is not exactly symmetric, and for factors with a 1e-6 spectral range using
+// the mirror element was measured to move the smallest eigenvalues by 3e-3) from split-K partials (column-major,
+// so consecutive i are contiguous); the association ((s0 + s1) + (s2 + s3)) with s_r summing slices r, r+4, ... is
+// the one of tc_gemm.cu's tc_reduce_kernel.
+__device__ __forceinline__ float gram_from_parts(const CholDesc& cd, int i, int j) {
+    const long long ww = (long long)cd.w * cd.w;
+    const float* p = cd.part + (long long)j * cd.w + i;
+    float s0 = p[0], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int k = 1;
+    for (; k + 3 < cd.nslices; k += 4) {
+        s0 += p[k * ww]; s1 += p[(k + 1) * ww]; s2 += p[(k + 2) * ww]; s3 += p[(k + 3) * ww];
+    }
+    for (; k < cd.nslices; ++k) s0 += p[k * ww];
+    return (s0 + s1) + (s2 + s3);
+}
+
 template <class T> struct Vec4T;
 template <> struct Vec4T<float> { using type = float4; };
 template <> struct Vec4T<double> { using type = double4; };
@@ -137,7 +153,8 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
     const TG* G = static_cast<const TG*>(cd.G);
     bool async_load = false;
     if constexpr (kSmem && sizeof(TG) == sizeof(T)) {
-        async_load = ((cd.ldg * (long long)sizeof(T)) & 15) == 0 && (((uintptr_t)G) & 15) == 0 && cd.ldg >= rup4(n);
+        async_load = !cd.part && ((cd.ldg * (long long)sizeof(T)) & 15) == 0 && (((uintptr_t)G) & 15) == 0 &&
+                     cd.ldg >= rup4(n);
         if (async_load) {
             constexpr int E = 16 / sizeof(T);
             for (int i = warp; i < n; i += nwarp) {
@@ -157,7 +174,8 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
     if (!async_load) {
         for (int i = warp; i < n; i += nwarp) {
             T* row = L + prow(i);
-            for (int j = lane; j < rup4(i + 1); j += 32) row[j] = (j <= i) ? T(G[(long long)i * cd.ldg + j]) : T(0);
+            for (int j = lane; j < rup4(i + 1); j += 32)
+                row[j] = (j <= i) ? (cd.part ? T(gram_from_parts(cd, i, j)) : T(G[(long long)i * cd.ldg + j])) : T(0);
         }
     }
     for (int i = tid; i < n; i += nthr) defic[i] = 0;
@@ -638,10 +656,24 @@ __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
         if (boff[b] < 0) continue;
         const int J0 = b * kNB, nb = min(kNB, n - J0), pb = cc_pitch(b);
         T* rb = rows + boff[b];
-        for (int r = warp; r < nb; r += kCcThreads / 32) {
-            const int i = J0 + r;
-            for (int j = lane; j < pb; j += 32) rb[r * pb + j] = (j <= i) ? T(G[(long long)i * cd.ldg + j]) : T(0);
-            if (lane == 0) { diag0[i] = (float)G[(long long)i * cd.ldg + i]; defic[i] = 0; }
+        if (cd.part) {  // lane = row: the column-major partials are read 128 bytes per warp access
+            const int r = lane, i = J0 + r;
+            for (int j = warp; j < pb; j += kCcThreads / 32) {
+                if (r < nb) {
+                    const T g = (j <= i) ? T(gram_from_parts(cd, i, j)) : T(0);
+                    rb[r * pb + j] = g;
+                    if (j == i) { diag0[i] = (float)g; defic[i] = 0; }
+                }
+            }
+        } else {
+            for (int r = warp; r < nb; r += kCcThreads / 32) {
+                const int i = J0 + r;
+                for (int j = lane; j < pb; j += 32) {
+                    const T g = (j <= i) ? T(G[(long long)i * cd.ldg + j]) : T(0);
+                    rb[r * pb + j] = g;
+                    if (j == i) { diag0[i] = (float)g; defic[i] = 0; }
+                }
+            }
         }
     }
     CHOL_PHASE(0);

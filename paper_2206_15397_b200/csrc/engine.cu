@@ -366,6 +366,11 @@ void Plan::build_decomp_stages() {
         }
         // complete_[dir] completes the output of orth(src = dir), i.e. role S[dir ^ 1]
         upload(d_complete_[dir], comp);
+        static const bool fuse_gram = [] {
+            const char* e = std::getenv("RKFAC_GRAM_FUSED");
+            return !(e && e[0] == '0');
+        }();
+        gram_[dir]->set_defer_reduce(fuse_gram);  // the Cholesky-inverse sums the Gram's K slices while loading it
         xq_[dir]->finalize(); xqf_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
@@ -377,14 +382,20 @@ void Plan::build_decomp_stages() {
     }
     upload(d_copy_ut_, cp);
     copy_ut_total_ = cp_off;
-    std::vector<CholDesc> c64, c32;
+    std::vector<CholDesc> c64, c32[2];
     std::vector<EigDesc> eg;
     std::vector<PostDesc> po;
     std::vector<CompleteDesc> cu;
     std::vector<BracketDesc> br;
     for (auto& F : f_) {
-        c64.push_back(CholDesc{F.w, F.G64, F.wp, F.Linv64, F.wp, nullptr, F.flags, F.flags + F.w, F.chol_scratch});
-        c32.push_back(CholDesc{F.w, F.G32, F.wp, F.Linv32, F.wp, F.Linv32lo, F.flags, F.flags + F.w, F.chol_scratch});
+        c64.push_back(CholDesc{F.w, F.G64, F.wp, F.Linv64, F.wp, nullptr, F.flags, F.flags + F.w, F.chol_scratch,
+                               nullptr, 1});
+        for (int dir = 0; dir < 2; ++dir) {
+            auto sp = gram_[dir]->split_of((int)(&F - f_.data()));
+            if (!gram_[dir]->defer_reduce()) sp = {nullptr, 1};
+            c32[dir].push_back(CholDesc{F.w, F.G32, F.wp, F.Linv32, F.wp, F.Linv32lo, F.flags, F.flags + F.w,
+                                        F.chol_scratch, sp.first, sp.second});
+        }
         EigDesc e{};
         e.n = F.w; e.r = F.r; e.A = F.core; e.lda = F.w; e.scratch = F.eig_scratch; e.refl = F.refl;
         e.tau = F.tau; e.dvec = F.dvec; e.evec = F.evec; e.evals = F.evals; e.scr = F.scr; e.piv = F.piv;
@@ -395,7 +406,8 @@ void Plan::build_decomp_stages() {
         br.push_back(BracketDesc{F.r, F.dvals, F.bracket});
     }
     upload(d_chol64_, c64);
-    upload(d_chol32_, c32);
+    upload(d_chol32_[0], c32[0]);
+    upload(d_chol32_[1], c32[1]);
     upload(d_eig_, eg);
     upload(d_post_, po);
     upload(d_complete_u_, cu);
@@ -514,7 +526,7 @@ void Plan::orth(int src, bool fp64, cudaStream_t s) {
         tri64_[src]->launch(s);
     } else {
         gram_[src]->launch(s);
-        launch_cholinv(d_chol32_.as<CholDesc>(), n, wmax_, false, false, kTol32, s);
+        launch_cholinv(d_chol32_[src].as<CholDesc>(), n, wmax_, false, false, kTol32, s);
         tri_[src]->launch(s);
     }
     // rank-deficient columns stay zero here; the final basis is completed in decompose()

@@ -138,7 +138,7 @@ class Plan {
     std::unique_ptr<TcGemm> ea_tc_stage_;
     std::unique_ptr<GemmBatch> ea_simt_;
     std::unique_ptr<TcGemm> ap_[4];
-    DevBuf d_omega_, d_chol64_, d_chol32_, d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
+    DevBuf d_omega_, d_chol64_, d_chol32_[2], d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
     DevBuf d_split_x_, d_split_m_, d_split_omega_, d_split_j_, d_copy_ut_;
     long long split_x_total_ = 0, split_m_total_ = 0, split_j_total_ = 0, copy_ut_total_ = 0;
     std::vector<OmegaDesc> omega_;

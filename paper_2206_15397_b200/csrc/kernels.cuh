@@ -32,6 +32,10 @@ struct CholDesc {
     int* flags;      // w rank-deficiency flags
     int* nflags;     // any flag
     void* scratch;   // global fallback for the packed triangle
+    // Split-K Gram (FP32 only): when part != nullptr, G is the fixed-order sum of nslices column-major w x w partials
+    // (slice s, element (m, n) at part[s * w * w + n * w + m]; tc_gemm.cu's reduction order), formed while loading
+    const float* part;
+    int nslices;
 };
 size_t cholinv_smem_bytes(int wmax, bool fp64);
 void launch_cholinv(const CholDesc* d_descs, int nfactors, int wmax, bool fp64, bool gram64, double tol,

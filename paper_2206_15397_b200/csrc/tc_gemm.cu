@@ -1001,7 +1001,7 @@ void TcGemm::launch(cudaStream_t s) const {
                                      d_begin_.as<int>());
     count_launch();
     RKFAC_CHECK_LAUNCH();
-    if (any_split_) {
+    if (any_split_ && !defer_reduce_) {
         const int blocks = (int)std::min<long long>(red_total_, kNumSMs * 8);
         tc_reduce_kernel<<<blocks, 256, 0, s>>>(d_probs_.as<TcProb>(), d_red_.as<TcRed>(), nred_, red_total_);
         count_launch();

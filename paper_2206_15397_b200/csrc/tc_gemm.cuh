@@ -11,6 +11,7 @@
 
 #include <cuda.h>
 
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -64,6 +65,14 @@ class TcGemm {
   public:
     int add(const TcProblemDesc& d);
     void set_max_ctas(int n) { cap_ = n; }  // persistent-grid cap (0: all SMs); leaves SMs to concurrent streams
+    // the consumer reduces the split-K partials itself (launch() skips the reduction kernel); after finalize(),
+    // split_of(prob) gives the partial buffer and slice count of a problem ({nullptr, 1} when it was not split)
+    void set_defer_reduce(bool on) { defer_reduce_ = on; }
+    bool defer_reduce() const { return defer_reduce_; }
+    std::pair<const float*, int> split_of(int prob) const {
+        const TcProb& p = probs_[prob];
+        return p.ksplit > 1 ? std::make_pair((const float*)p.partial, p.ksplit) : std::make_pair((const float*)nullptr, 1);
+    }
     void finalize();
     void launch(cudaStream_t s) const;
     bool empty() const { return tiles_.empty(); }
@@ -78,7 +87,8 @@ class TcGemm {
     int nctas_ = 0;
     bool any_split_ = false;
     int cfg_ = 0;
-    int cap_ = 0;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
+    int cap_ = 0;
+    bool defer_reduce_ = false;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
     int nred_ = 0;
     long long red_total_ = 0;
     DevBuf d_probs_, d_maps_, d_tiles_, d_begin_, partials_, d_red_;
