@@ -314,8 +314,13 @@ def run_ours(args, wl):
     send = torch.zeros(layout.chunk, dtype=torch.float32, device=dev)
     recv = torch.empty(world * layout.chunk, dtype=torch.float32, device=dev)
 
+    graph = None  # CUDA graph of the whole step (rk.StepGraph), captured after the eager warm-up
+
     def one_step():
-        step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
+        if graph is not None:
+            graph.replay()
+        else:
+            step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
         for i, l in enumerate(mine):
             send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
         if world > 1:
@@ -331,6 +336,13 @@ def run_ours(args, wl):
         reset()
         one_step()
     torch.cuda.synchronize()
+    if args.graph:
+        reset()
+        graph = rk.StepGraph(step, OMEGA_ROOT, 0, lam, 0.95, 1.0)
+        for _ in range(2):  # replays are warmed too
+            reset()
+            one_step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
@@ -358,7 +370,7 @@ def run_ours(args, wl):
     torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
-    launches = ctx.launches() - launches0
+    launches = ctx.launches() - launches0 + (graph.launches * args.steps if graph is not None else 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms_local = sum(step_ms) / len(step_ms)
     # per-stage timing and the roofline: the single plan (all factors per launch), K more steps, untimed above
@@ -389,7 +401,13 @@ def run_ours(args, wl):
                 ds.copy_(hs, non_blocking=True)
             for hg, dg in zip(h_grads, step.grads):
                 dg.copy_(hg, non_blocking=True)
-            one_step()
+            step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)  # eager here: the whole e2e step is captured as one graph
+            for i, l in enumerate(mine):
+                send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
+            if world > 1:
+                dist.all_gather_into_tensor(recv, send)
+            else:
+                recv.copy_(send)
             for ho, do in zip(h_outs, step.outs):
                 ho.copy_(do, non_blocking=True)
             return
@@ -509,6 +527,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=2, help="layer groups on concurrent streams (StreamedStep)")
     ap.add_argument("--profile-step", action="store_true", help="run one step under cudaProfilerStart/Stop and exit")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
+                    help="replay the timed step as one CUDA graph (rk.StepGraph); measured within 0.5 %% of eager")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -138,6 +138,9 @@ int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t rng_ro
  * and 7 counts indexed: 0 EA update, 1 decomposition, 2 preconditioning, 3 X*Q products (the GEMM stage),
  * 4 orthonormalisations, 5 core + eigensolve + lift, 6 whole step. */
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
+/* Build every stage rkfac_plan_step(rho, scale, *, *, lambda) uses without launching anything, so the step only
+ * enqueues kernels and may be captured into a CUDA graph (the Omega seed is a kernel argument: capture per step id). */
+int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambda);
 /* Cap the persistent tensor-core grids of this plan at `ctas` CTAs (0: one per SM), leaving SMs to the
  * latency-bound per-factor kernels of plans running concurrently on other streams (StreamedStep). */
 int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas);

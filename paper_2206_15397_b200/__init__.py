@@ -113,6 +113,7 @@ SIGNATURES = {
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "rkfac_plan_set_timing": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_set_max_ctas": (C.c_int, [_vp, C.c_int]),
+    "rkfac_plan_prepare": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double]),
 }
 
 
@@ -463,6 +464,12 @@ class BatchedStep:
         _check(self.ctx.lib.rkfac_plan_step(self.h, rho, scale, _c_u64(rng_root), _c_u64(step), lam), self.ctx.h,
                "plan_step")
 
+    def prepare(self, lam: float, rho: float = 0.95, scale: float = 1.0):
+        """Build every stage step(lam, rho, scale) uses, without launching (so the step can be graph-captured)."""
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        _check(self.ctx.lib.rkfac_plan_prepare(self.h, rho, scale, lam), self.ctx.h, "plan_prepare")
+
     def set_timing(self, on: bool):
         _check(self.ctx.lib.rkfac_plan_set_timing(self.h, 1 if on else 0), self.ctx.h, "set_timing")
 
@@ -487,6 +494,35 @@ class BatchedStep:
 
 
 STREAMED_TC_CTAS = 132
+
+
+class StepGraph:
+    """One full preconditioned step (EA -> rand-EVD -> precondition of every layer, every group's stream) captured
+    once as a CUDA graph and replayed: ~70 dependent launches per group chain are submitted as one graph launch, so the
+    inter-kernel gaps and the host enqueue cost leave the step.  Stages are built by ``prepare`` first (capture only
+    enqueues kernels); the Omega seeds (rng_root, step) are baked in, so capture one graph per step id (or reuse one
+    when the step id is fixed, as in bench.py).  Replays read the current contents of the step's device buffers
+    (factors, samples, grads) and are bitwise identical to ``step_obj.step``.
+    """
+
+    def __init__(self, step_obj, rng_root: int, step: int, lam: float, rho: float = 0.95, scale: float = 1.0):
+        torch = _torch()
+        self.step_obj = step_obj
+        step_obj.prepare(lam, rho, scale)
+        dev = step_obj.device
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        n0 = step_obj.ctx.launches()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                step_obj.step(rng_root, step, lam, rho, scale)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        self.launches = step_obj.ctx.launches() - n0  # kernels per replay
+
+    def replay(self):
+        self.graph.replay()
 
 
 class StreamedStep:
@@ -578,6 +614,10 @@ class StreamedStep:
         if lam <= 0.0:
             raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
         self._fan_out(lambda s: s.step(rng_root, step, lam, rho, scale))
+
+    def prepare(self, lam: float, rho: float = 0.95, scale: float = 1.0):
+        for sub in self.subs:
+            sub.prepare(lam, rho, scale)
 
     def lowrank(self, f: int) -> LowRankEig:
         s, j = self._owner[f]

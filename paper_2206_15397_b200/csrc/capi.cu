@@ -308,6 +308,10 @@ int rkfac_plan_timing(rkfac_plan_t plan, float* sums_ms, int* counts) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->timing_report(sums_ms, counts); });
 }
 
+int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambda) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->prepare(rho, scale, lambda); });
+}
+
 int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas) {
     return guarded(plan ? plan->ctx : nullptr, [&] {
         RKFAC_REQUIRE(ctas >= 0, RKFAC_INVALID_ARGUMENT, "negative CTA cap");

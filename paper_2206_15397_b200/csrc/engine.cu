@@ -647,6 +647,12 @@ void Plan::precondition(double lambda) {
     mark(kApply, false);
 }
 
+void Plan::prepare(double rho, double scale, double lambda) {
+    RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
+    if (samples_bound_ && (rho != ea_rho_ || scale != ea_scale_)) build_ea_stage(rho, scale);
+    if (!layers_.empty() && lambda != ap_lambda_) build_apply_stages(lambda);
+}
+
 void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double lambda) {
     RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
     mark(kStep, true);

@@ -100,6 +100,9 @@ class Plan {
     void decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh = false);
     void precondition(double lambda);
     void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
+    // Builds every stage a step with these parameters uses (descriptor uploads), so that the step itself only
+    // enqueues kernels and can be captured into a CUDA graph.
+    void prepare(double rho, double scale, double lambda);
 
     enum TimingKind { kEA = 0, kDecompose = 1, kApply = 2, kXQ = 3, kOrth = 4, kEig = 5, kStep = 6, kTimingKinds = 7 };
     void set_timing(bool on) { timing_ = on; timing_reset(); }
