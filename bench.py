@@ -401,7 +401,7 @@ def run_ours(args, wl):
                 ds.copy_(hs, non_blocking=True)
             for hg, dg in zip(h_grads, step.grads):
                 dg.copy_(hg, non_blocking=True)
-            step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)  # eager here: the whole e2e step is captured as one graph
+            step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
             for i, l in enumerate(mine):
                 send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
             if world > 1:
@@ -411,27 +411,9 @@ def run_ours(args, wl):
             for ho, do in zip(h_outs, step.outs):
                 ho.copy_(do, non_blocking=True)
             return
-        # per group on its own stream: its inputs' H2D, its step, its results' D2H -- one group's copies overlap
-        # the other group's kernels
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        joins = []
-        for sub, st, part in zip(step.subs, step.streams, step.parts):
-            st.wait_event(fork)
-            with torch.cuda.stream(st):
-                for i, l in enumerate(part):
-                    for w in (0, 1):
-                        sub.samples[2 * i + w].copy_(h_samples[2 * l + w], non_blocking=True)
-                    sub.grads[i].copy_(h_grads[l], non_blocking=True)
-                sub.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
-                for i, l in enumerate(part):
-                    h_outs[l].copy_(sub.outs[i], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(st)
-                joins.append(ev)
-        for ev in joins:
-            stream.wait_event(ev)
-        step.ctx.sync_stream()
+        # the public host-buffer step: per group, samples H2D -> EA -> rand-EVD while the gradients upload on a copy
+        # stream, then precondition -> results D2H (one group's copies overlap the other group's kernels)
+        step.step_host(OMEGA_ROOT, 0, lam, h_samples, h_grads, h_outs, 0.95, 1.0)
         for i, l in enumerate(mine):
             send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
         if world > 1:

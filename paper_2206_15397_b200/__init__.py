@@ -619,6 +619,53 @@ class StreamedStep:
         for sub in self.subs:
             sub.prepare(lam, rho, scale)
 
+    def step_host(self, rng_root: int, step: int, lam: float, h_samples, h_grads, h_outs, rho: float = 0.95,
+                  scale: float = 1.0):
+        """The step with its inputs and outputs in (pinned) host memory, in the original factor / layer order.
+
+        Per group, on the group's stream: H2D of its samples -> EA -> rand-EVD; meanwhile a copy stream brings its
+        gradients (needed only by the preconditioning); then precondition -> D2H of its results.  One group's copies
+        overlap the other groups' kernels, and every gradient upload overlaps its own group's decomposition.
+        """
+        if lam <= 0.0:
+            raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
+        torch = _torch()
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = [torch.cuda.Stream(device=self.device) for _ in self.subs]
+        main = torch.cuda.current_stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        joins = []
+        for sub, st, cp, part in zip(self.subs, self.streams, self._copy_streams, self.parts):
+            st.wait_event(fork)
+            with torch.cuda.stream(st):
+                for i, l in enumerate(part):
+                    for w in (0, 1):
+                        if sub.samples:
+                            sub.samples[2 * i + w].copy_(h_samples[2 * l + w], non_blocking=True)
+                got_samples = torch.cuda.Event()
+                got_samples.record(st)
+            cp.wait_event(got_samples)  # the gradients follow the samples on the copy engine
+            with torch.cuda.stream(cp):
+                for i, l in enumerate(part):
+                    sub.grads[i].copy_(h_grads[l], non_blocking=True)
+                got_grads = torch.cuda.Event()
+                got_grads.record(cp)
+            with torch.cuda.stream(st):
+                if sub.samples:
+                    sub.ea_update(rho, scale)
+                sub.decompose(rng_root, step)
+                st.wait_event(got_grads)
+                sub.precondition(lam)
+                for i, l in enumerate(part):
+                    h_outs[l].copy_(sub.outs[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                joins.append(ev)
+        for ev in joins:
+            main.wait_event(ev)
+        self.ctx.sync_stream()
+
     def lowrank(self, f: int) -> LowRankEig:
         s, j = self._owner[f]
         return self.subs[s].lowrank(j)

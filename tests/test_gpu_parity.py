@@ -397,3 +397,37 @@ def test_streamed_step_is_bitwise_the_batched_step(cuda):
         assert torch.equal(one.bases_t[f], two.bases_t[f]) and torch.equal(one.dvals[f], two.dvals[f])
     for l in range(len(layers)):
         assert torch.equal(one.outs[l], two.outs[l])
+
+
+def test_streamed_step_from_host_buffers_is_bitwise_the_step(cuda):
+    """StreamedStep.step_host (pinned host inputs/outputs, gradients uploaded during the decomposition) == step()."""
+    import math
+
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    layers = [rk.LayerSpec(577, 64), rk.LayerSpec(300, 257), rk.LayerSpec(28, 64)]
+    kw = dict(rank=40, oversampling=10, power_iters=2, method=rk.DecompMethod.SREVD, n_samples=[64], device=0)
+    st = rk.StreamedStep(layers, groups=2, **kw)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    h_samples, h_grads = [], []
+    for f, d in enumerate(st.dims):
+        s = torch.arange(1, d + 1, device=cuda, dtype=torch.float32).pow(-1.0)
+        h_samples.append((torch.randn(d, 64, device=cuda, generator=g) * s[:, None] / math.sqrt(64)).cpu().pin_memory())
+    for L in layers:
+        h_grads.append(torch.randn(L.dim_g, L.dim_a, device=cuda, generator=g).cpu().pin_memory())
+    h_outs = [torch.empty(L.dim_g, L.dim_a).pin_memory() for L in layers]
+    x0 = [x.clone() for x in st.factors]
+    st.step_host(7, 0, 0.1, h_samples, h_grads, h_outs)
+    torch.cuda.synchronize()
+    got = [o.clone() for o in h_outs]
+    for x, y in zip(st.factors, x0):
+        x.copy_(y)
+    for f in range(len(st.dims)):
+        st.samples[f].copy_(h_samples[f])
+    for l in range(len(layers)):
+        st.grads[l].copy_(h_grads[l])
+    st.step(7, 0, 0.1)
+    torch.cuda.synchronize()
+    for l in range(len(layers)):
+        assert torch.equal(got[l], st.outs[l].cpu())
