@@ -993,47 +993,76 @@ __global__ void __launch_bounds__(kVecThreads) eigvec_kernel(const EigDesc* __re
 #undef W_
 }
 
-// Re-orthogonalise clusters of (numerically) equal eigenvalues: MGS by one warp per factor (clusters are rare;
-// the scan is O(r)).
-__global__ void __launch_bounds__(32) reorth_kernel(const EigDesc* __restrict__ descs) {
+// Re-orthogonalise clusters of (numerically) equal eigenvalues, one CTA per factor.  Clusters are rare in general
+// but large right after a zero-init EA (rank(X) < w: ~w - rank eigenvalues at 0), so every vector of a
+// cluster is orthogonalised against all earlier ones at once -- classical Gram-Schmidt applied twice (CGS2): thread
+// per earlier vector for the coefficients, thread per component for the update -- O(c) block steps instead of the
+// O(c^2) dependent warp dot products of MGS.  The cluster is staged in shared memory when it fits (n*c <= kRoElems).
+constexpr int kRoThreads = 256;
+constexpr int kRoElems = 24576;  // 192 KB of FP64
+
+__global__ void __launch_bounds__(kRoThreads) reorth_kernel(const EigDesc* __restrict__ descs) {
     const EigDesc& ed = descs[blockIdx.x];
     const int n = ed.n, r = ed.r;
-    __shared__ double d[kMaxN], e[kMaxN], lam[kMaxN], bnd[3];
+    __shared__ double d[kMaxN], e[kMaxN], lam[kMaxN], coef[kMaxN], bnd[3], red[33];
+    __shared__ int any_s;
+    extern __shared__ double zc[];  // staged cluster, [t][c] (row t = component)
     const int tid = threadIdx.x;
-    for (int i = tid; i < n; i += 32) {
+    for (int i = tid; i < n; i += kRoThreads) {
         d[i] = ed.dvec[i];
         e[i] = (i < n - 1) ? ed.evec[i] : 0.0;
     }
-    for (int i = tid; i < r; i += 32) lam[i] = ed.evals[i];
-    __syncwarp();
-    tri_bounds(d, e, n, bnd);
-    __syncwarp();
+    for (int i = tid; i < r; i += kRoThreads) lam[i] = ed.evals[i];
+    if (tid == 0) any_s = 0;
+    __syncthreads();
+    if (tid < 32) tri_bounds(d, e, n, bnd);
+    __syncthreads();
     const double clus = 1e-10 * bnd[2];
-    bool any = false;
-    for (int i = tid + 1; i < r; i += 32) any |= fabs(lam[i - 1] - lam[i]) <= clus;
-    if (!__any_sync(0xffffffffu, any)) return;
+    for (int i = tid + 1; i < r; i += kRoThreads)
+        if (fabs(lam[i - 1] - lam[i]) <= clus) any_s = 1;
+    __syncthreads();
+    if (!any_s) return;
     const long long S = r;
     double* Z = ed.z;
     int k = 0;
     while (k < r) {
         int k1 = k + 1;
         while (k1 < r && fabs(lam[k1 - 1] - lam[k1]) <= clus) ++k1;
-        for (int pass = 0; pass < 2 && k1 - k > 1; ++pass) {
-            for (int j = k; j < k1; ++j) {
-                for (int i = k; i < j; ++i) {
-                    double dot = 0.0;
-                    for (int t = tid; t < n; t += 32) dot += Z[t * S + i] * Z[t * S + j];
-                    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                    for (int t = tid; t < n; t += 32) Z[t * S + j] -= dot * Z[t * S + i];
-                    __syncwarp();
+        const int c = k1 - k;
+        if (c > 1) {
+            const bool staged = (long long)n * c <= kRoElems;
+            // element (t, i) of the cluster (i relative to k)
+            auto at = [&](int t, int i) -> double& { return staged ? zc[t * c + i] : Z[t * S + k + i]; };
+            if (staged)
+                for (int x = tid; x < n * c; x += kRoThreads) zc[x] = Z[(x / c) * S + k + (x % c)];
+            __syncthreads();
+            for (int j = 0; j < c; ++j) {
+                for (int pass = 0; pass < 2 && j > 0; ++pass) {
+                    for (int i = tid; i < j; i += kRoThreads) {
+                        double s0 = 0.0, s1 = 0.0;
+                        int t = 0;
+                        for (; t + 1 < n; t += 2) { s0 += at(t, i) * at(t, j); s1 += at(t + 1, i) * at(t + 1, j); }
+                        if (t < n) s0 += at(t, i) * at(t, j);
+                        coef[i] = s0 + s1;
+                    }
+                    __syncthreads();
+                    for (int t = tid; t < n; t += kRoThreads) {
+                        double acc = at(t, j);
+                        for (int i = 0; i < j; ++i) acc -= coef[i] * at(t, i);
+                        at(t, j) = acc;
+                    }
+                    __syncthreads();
                 }
                 double nn = 0.0;
-                for (int t = tid; t < n; t += 32) nn += Z[t * S + j] * Z[t * S + j];
-                for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+                for (int t = tid; t < n; t += kRoThreads) nn += at(t, j) * at(t, j);
+                nn = block_sum_d(nn, red);
                 const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-                for (int t = tid; t < n; t += 32) Z[t * S + j] *= inv;
-                __syncwarp();
+                for (int t = tid; t < n; t += kRoThreads) at(t, j) *= inv;
+                __syncthreads();
             }
+            if (staged)
+                for (int x = tid; x < n * c; x += kRoThreads) Z[(x / c) * S + k + (x % c)] = zc[x];
+            __syncthreads();
         }
         k = k1;
     }
@@ -1319,7 +1348,9 @@ void launch_eig(const EigDesc* d_descs, int nfactors, int nmax, int rmax, cudaSt
                     s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
-    reorth_kernel<<<nfactors, 32, 0, s>>>(d_descs);
+    RKFAC_CUDA(cudaFuncSetAttribute(reorth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kRoElems * sizeof(double))));
+    reorth_kernel<<<nfactors, kRoThreads, kRoElems * sizeof(double), s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
     dim3 grid((unsigned)ceil_div(std::max(rmax, 1), kBxCols), (unsigned)nfactors);
