@@ -56,6 +56,8 @@ TcOut out_t(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 1; retu
 // 1.4e-5, orthonormality 1.1e-4 -> 7.8e-6.
 constexpr int kSliceK = 512;
 constexpr int kSliceKFinal = 1024;
+// the apply's long-K products write d_G x r partials per slice (1 GB per layer at d = 16384 with 512-slices)
+constexpr int kSliceKApply = 2048;
 
 TcOut out_r(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 0; return o; }
 
@@ -488,7 +490,7 @@ void Plan::build_apply_stages(double lambda) {
         p0.B = A.Uti; p0.B_lo = A.Utilo; p0.ldb = A.dp;
         p0.cs = A.bracket;
         p0.out0 = out_r(L.W1, A.rp); p0.lo0 = out_r(L.W1lo, A.rp);
-        p0.slice_k = kSliceK;
+        p0.slice_k = kSliceKApply;
         ap_[0]->add(p0);
         TcProblemDesc p1;
         p1.M = G.d; p1.N = A.d; p1.K = A.r;
@@ -503,7 +505,7 @@ void Plan::build_apply_stages(double lambda) {
         p2.B = L.Mt; p2.B_lo = L.Mtlo; p2.ldb = dGp;
         p2.rs = G.bracket;
         p2.out0 = out_t(L.W2t, G.rp); p2.lo0 = out_t(L.W2tlo, G.rp);
-        p2.slice_k = kSliceK;
+        p2.slice_k = kSliceKApply;
         ap_[2]->add(p2);
         TcProblemDesc p3;
         p3.M = G.d; p3.N = A.d; p3.K = G.r;
