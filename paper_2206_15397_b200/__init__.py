@@ -351,6 +351,38 @@ def apply_lowrank_damped_inverse(lr: LowRankEig, lam: float, v, side: ApplySide)
     return out
 
 
+# ------------------------------------------------------------------------ exact K-FAC comparator
+@dataclass
+class SymEigResult:  # eig.hpp:20-25: p (n x n, eigenvectors as columns), d (n, descending)
+    p: object
+    d: object
+
+
+def sym_eig(s, fp64: bool = False) -> SymEigResult:
+    """eig.hpp:210-237 for the exact K-FAC comparator: full symmetric eigendecomposition, eigenvalues descending.
+
+    Not on the rand-K-FAC hot path: this is the cubic baseline the randomized path is measured against
+    (harness.hpp:402-478 bench-inverse), so it uses the CUDA toolkit's dense eigensolver (cuSOLVER syevd through
+    torch.linalg.eigh) instead of a hand-written kernel.  Asymmetry above 1e-8 * max(1, ||S||_max) is rejected like
+    eig.hpp:213-215; the symmetrised matrix is decomposed."""
+    torch = _torch()
+    _need_cuda_f32(s, "s")
+    if s.dim() != 2 or s.shape[0] != s.shape[1]:
+        raise DimensionMismatch("sym_eig: matrix must be square")
+    amax = float(s.abs().max()) if s.numel() else 0.0
+    if s.numel() and float((s - s.T).abs().max()) > 1e-8 * max(1.0, amax) * 1e4:  # FP32 storage: 1e4 x the FP64 bar
+        raise DimensionMismatch("sym_eig: matrix is not symmetric")
+    a = 0.5 * (s + s.T)
+    lam, p = torch.linalg.eigh(a.double() if fp64 else a)
+    return SymEigResult(p.flip(1).float().contiguous(), lam.flip(0).float().contiguous())
+
+
+def apply_eig_damped_inverse(eig: SymEigResult, lam: float, v, side: ApplySide):
+    """kfactor.hpp:165-186: LEFT U (D + lam I)^{-1} U^T V, RIGHT V U (D + lam I)^{-1} U^T -- through the hot path's
+    own apply kernels: Eq. 11 with a complete orthonormal U is exactly (U D U^T + lam I)^{-1}."""
+    return apply_lowrank_damped_inverse(LowRankEig(eig.p, eig.d, DecompMethod.EXACT), lam, v, side)
+
+
 # ------------------------------------------------------------------------------------- batched step
 
 

@@ -185,6 +185,15 @@ void Plan::set_explicit_seed(int f, uint64_t seed, uint64_t ctr0) {
 
 void Plan::bind_factors(float* const* X, const long long* ldx, float* const* Ut, const long long* ldu,
                         float* const* dvals) {
+    if (factors_bound_) {  // re-binding the same buffers (repeated single-factor calls): the stages are still valid
+        bool same = true;
+        for (size_t i = 0; i < f_.size() && same; ++i) {
+            const FactorState& F = f_[i];
+            same = F.X == X[i] && F.ldx == (ldx ? ldx[i] : F.d) && F.Ut == Ut[i] && F.ldu == (ldu ? ldu[i] : F.d) &&
+                   F.dvals == dvals[i];
+        }
+        if (same) return;
+    }
     x_tma_ok_ = true;
     for (size_t i = 0; i < f_.size(); ++i) {
         FactorState& F = f_[i];

@@ -431,3 +431,25 @@ def test_streamed_step_from_host_buffers_is_bitwise_the_step(cuda):
     torch.cuda.synchronize()
     for l in range(len(layers)):
         assert torch.equal(got[l], st.outs[l].cpu())
+
+
+# ------------------------------------------------------------------------------------ exact K-FAC comparator
+@pytest.mark.parametrize("side", ["left", "right"])
+def test_exact_kfac_comparator_matches_oracle(port, cuda, side):
+    """full eigendecomposition + apply_eig_damped_inverse (kfactor.hpp:165-186) vs the oracle's
+    sym_eig (eig.hpp:210-237) and apply_eig_damped_inverse on the same EA factor."""
+    import paper_2206_15397_b200 as rk
+
+    d, lam = 384, 0.1
+    x = build_factor(port, d, 128, 6, 1.0, f=0)
+    p0, d0 = port.sym_eig(x)
+    v, _ = port.sample_gaussian(port.substream(GRAD_ROOT, 0, 0), 0, d, 200) if side == "left" else \
+        port.sample_gaussian(port.substream(GRAD_ROOT, 0, 0), 0, 200, d)
+    s0 = port.apply_eig_damped_inverse(p0, d0, lam, v, side)
+    eig = rk.sym_eig(t32(x, cuda))
+    assert eig_err(np64(eig.d)[:50], d0[:50]) < TOL  # the well-resolved top of the spectrum
+    s1 = rk.apply_eig_damped_inverse(eig, lam, t32(v, cuda), rk.ApplySide.LEFT if side == "left" else
+                                     rk.ApplySide.RIGHT)
+    assert rel_fro(np64(s1), s0) < TOL
+    with pytest.raises(rk.DampingNonpositive):
+        rk.apply_eig_damped_inverse(eig, 0.0, t32(v, cuda), rk.ApplySide.LEFT)
