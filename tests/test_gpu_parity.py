@@ -453,3 +453,56 @@ def test_exact_kfac_comparator_matches_oracle(port, cuda, side):
     assert rel_fro(np64(s1), s0) < TOL
     with pytest.raises(rk.DampingNonpositive):
         rk.apply_eig_damped_inverse(eig, 0.0, t32(v, cuda), rk.ApplySide.LEFT)
+
+
+# ------------------------------------------------------------------------------- optimizer orchestration
+@pytest.mark.parametrize("method", ["sre", "rs", "kfac"])
+def test_kfac_optimizer_cache_and_schedule_match_oracle(port, cuda, method):
+    """kfac.KfacOptimizer (identity-init EA through the plan, decomposition cache on T_KI) == the reference's
+    optimizer loop restated with the oracle (optimizer.hpp:139-167, network.hpp:155-165)."""
+    import math
+
+    import torch
+    import paper_2206_15397_b200 as rk
+    from paper_2206_15397_b200.kfac import KfacOptimizer, Method, OptimizerConfig, ScheduleOverrides
+
+    layers = [rk.LayerSpec(65, 48), rk.LayerSpec(49, 10)]
+    n, r, p, q, lam, seed = 32, 24, 6, 2, 0.1, 11
+    meth = {"sre": Method.SRE_KFAC, "rs": Method.RS_KFAC, "kfac": Method.KFAC}[method]
+    cfg = OptimizerConfig(method=meth, n_pwr_it=q,
+                          overrides=ScheduleOverrides(lam=lam, target_rank=r, oversampling=p, t_ki=10))
+    opt = KfacOptimizer(layers, cfg, n, rng_seed=seed)
+    xs = []
+    for L in layers:
+        xs += [np.eye(L.dim_a), np.eye(L.dim_g)]
+    cached = None
+    for k in range(2):
+        a_m, g_m, grads = [], [], []
+        for l, L in enumerate(layers):
+            a, _ = port.sample_gaussian(port.substream(3, k, 2 * l), 0, L.dim_a, n)
+            g, _ = port.sample_gaussian(port.substream(3, k, 2 * l + 1), 0, L.dim_g, n)
+            j, _ = port.sample_gaussian(port.substream(4, k, l), 0, L.dim_g, L.dim_a)
+            a_m.append(a); g_m.append(g); grads.append(j)
+            xs[2 * l] = port.ea_update(xs[2 * l], a / math.sqrt(n), 0.95)
+            xs[2 * l + 1] = port.ea_update(xs[2 * l + 1], g / math.sqrt(n), 0.95)
+        opt.accumulate_factors([t32(a, cuda) for a in a_m], [t32(g, cuda) for g in g_m])
+        outs = opt.step([t32(j, cuda) for j in grads], step=k)
+        if k == 0:  # step 0 % T_KI == 0: decompose; step 1 reuses the cached decompositions
+            cached = []
+            for f, x in enumerate(xs):
+                if method == "kfac":
+                    pm, dv = port.sym_eig(x)
+                    cached.append((pm, dv))
+                else:
+                    fn = port.srevd if method == "sre" else port.rsvd_psd
+                    u0, d0, _ = fn(x, r, p, q, port.substream(seed, k, f), 0)
+                    cached.append((u0, d0))
+        for l in range(len(layers)):
+            (ua, da), (ug, dg) = cached[2 * l], cached[2 * l + 1]
+            if method == "kfac":
+                m = port.apply_eig_damped_inverse(ua, da, lam, grads[l], "right")
+                s0 = port.apply_eig_damped_inverse(ug, dg, lam, m, "left")
+            else:
+                s0 = port.precondition(ua, da, ug, dg, lam, grads[l])
+            assert rel_fro(np64(outs[l]), s0) < TOL, (k, l)
+    assert opt.timings.decomposition > 0 and opt.timings.inverse_apply > 0
