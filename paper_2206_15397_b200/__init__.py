@@ -594,7 +594,20 @@ class StreamedStep:
                                          factor_indices=[tags[2 * l + w] for l in part for w in (0, 1)],
                                          max_ctas=max_ctas))
         self.ctx = self.subs[0].ctx
-        self.streams = [torch.cuda.Stream(device=device) for _ in self.subs]
+        # the group with the most decomposition work is the critical chain: its stream gets the highest priority so
+        # its kernels take SMs first when other groups' grids drain (RKFAC_STREAM_PRIORITY=0 disables)
+        gcost = [sum(costs[l] for l in part) for part in self.parts]
+        lo_pri, hi_pri = torch.cuda.Stream.priority_range()
+        use_pri = os.environ.get("RKFAC_STREAM_PRIORITY", "1") != "0"
+        order = sorted(range(len(self.parts)), key=lambda g: -gcost[g])
+        pri = [0] * len(self.parts)
+        if use_pri and len(self.parts) > 1:
+            graded = os.environ.get("RKFAC_STREAM_PRIORITY", "1") == "2"
+            for rank_, g in enumerate(order):
+                pri[g] = max(hi_pri, hi_pri + rank_) if graded else (hi_pri if rank_ == 0 else 0)
+                if pri[g] > lo_pri:
+                    pri[g] = lo_pri
+        self.streams = [torch.cuda.Stream(device=device, priority=pri[g]) for g in range(len(self.subs))]
         # views in the original order
         self.dims, self.factors, self.samples, self.bases_t, self.dvals, self.ranks = [], [], [], [], [], []
         self.grads, self.outs, self.mids = [None] * nl, [None] * nl, [None] * nl
