@@ -850,7 +850,11 @@ int TcGemm::add(const TcProblemDesc& d) {
     // tiles: M in 128-row tiles; N in <=256-row tiles (multiples of 16); sym: square 128x128 upper tiles
     int per, ntn;
     if (d.sym) { per = 128; ntn = (int)ceil_div(d.N, 128); }
-    else { ntn = (int)ceil_div(d.N, kMaxBN); per = (int)ceil_div(ceil_div(d.N, ntn), 16) * 16; }
+    else {
+        const int maxbn = d.max_n_tile > 0 ? std::min(kMaxBN, d.max_n_tile) : kMaxBN;
+        ntn = (int)ceil_div(d.N, maxbn);
+        per = (int)ceil_div(ceil_div(d.N, ntn), 16) * 16;
+    }
     p.n_tile = per;
     const int ntm = (int)ceil_div(d.M, kBM);
     const int mn_tiles = d.sym ? ntm * (ntm + 1) / 2 : ntm * ntn;

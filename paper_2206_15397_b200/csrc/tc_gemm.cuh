@@ -38,6 +38,7 @@ struct TcProblemDesc {
     int ksplit = 0;    // 0 = choose automatically
     int slice_k = 0;   // > 0: split K so no TMEM accumulation chain is longer than slice_k (accuracy)
     int single = 0;    // 1: one TF32 MMA per product (no lo terms) -- for products that only carry a subspace
+    int max_n_tile = 0;  // > 0: N tiles of at most this many columns (more, shorter tiles; same arithmetic)
 };
 
 struct TcProb {  // device copy
