@@ -390,9 +390,11 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     constexpr int kStageBytes = StageCfg<kCfg>::kStageBytes;
     constexpr int kSub = StageCfg<kCfg>::kSub;
     constexpr int kBTileS = StageCfg<kCfg>::kBTile;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                                           ~uintptr_t(1023));
+    // declared 16-byte aligned only: with __align__(1024) the compiler folds the runtime alignment below to 0
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // 1024-byte aligned base, derived by indexing the __shared__ array (integer round-trips of the address would
+    // lose the address space: every smem access below would compile to generic LD/ST)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStagesBytesMax);
     float (*stage_tiles)[32][36] =
         reinterpret_cast<float (*)[32][36]>(smem + kStagesBytesMax + kBarrierBytes);
