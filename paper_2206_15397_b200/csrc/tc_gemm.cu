@@ -546,7 +546,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         const int q = warp % 4;  // TMEM lane quadrant this warp may access
         int rr = 0;
         uint32_t uses[2] = {0u, 0u};
-        // kCfg 2: Cin chunks of this warp in (tile, chunk) order, prefetched by cp.async two chunks ahead into a
+        // kCfg 2: Cin chunks of this warp in (tile, chunk) order, prefetched by cp.async kCinRing-1 chunks ahead into a
         // ring of kCinRing swizzled slots (zero-filled past the matrix edge); the output chunk is written in place
         unsigned char* ring = smem + kEaRingOff + (warp - 2) * kCinRing * kChunkBytes;
         unsigned char* mir = smem + kEaMirOff + (warp - 2) * 2 * kChunkBytes;
@@ -571,10 +571,8 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
         int chunk_no = 0;  // chunks consumed by this warp
-        if constexpr (kCfg == 2) {
-            cin_issue(0);
-            cin_issue(1);
-        }
+        if constexpr (kCfg == 2)
+            for (int i = 0; i + 1 < kCinRing; ++i) cin_issue(i);  // kCinRing - 1 chunks ahead
         for (int t = t_begin; t < t_end; ++t) {
           const TcTile tl = tiles[t];
           const int nsub = (kPair && tl.pair) ? 2 : 1;
@@ -636,7 +634,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     // group (the next chunk's) is pending
                     const int slot = chunk_no % kCinRing;
                     unsigned char* cs = ring + slot * kChunkBytes;
-                    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCinRing - 2) : "memory");
                     __syncwarp();
 #pragma unroll
                     for (int j4 = 0; j4 < 32; j4 += 4) {
@@ -673,7 +671,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     }
                     __syncwarp();
-                    cin_issue((chunk_no + 2) % kCinRing);
+                    cin_issue((chunk_no + kCinRing - 1) % kCinRing);
                     ++chunk_no;
                     continue;
                 }
