@@ -380,6 +380,36 @@ template <int NT>
 __device__ __forceinline__ double vget(const double (&a)[NT], int j) {
     return __shfl_sync(0xffffffffu, sel_slot<NT>(a, j >> 5), j & 31);
 }
+// 1/x and 1/sqrt(x) for the per-column reflector: hardware approximations (rcp/rsqrt.approx.f64, ~2^-23) refined by
+// two Newton steps (~2^-92 before rounding): within an ulp of the IEEE results at a fraction of their latency, which
+// sits on the serial chain of every column (x > 0, normal).
+__device__ __forceinline__ double rcp_fast(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-x, y, 1.0), y);
+    y = fma(y, fma(-x, y, 1.0), y);
+    return y;
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+    double y;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y;
+}
+
+template <int NT>
+__device__ __forceinline__ double tree_sum(const double (&a)[NT]) {
+    double t[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) t[i] = a[i];
+#pragma unroll
+    for (int w = 1; w < NT; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < NT; i += 2 * w) t[i] += t[i + w];
+    return t[0];
+}
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -458,22 +488,29 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
     double V[NT], W[NT], Vn[NT];
     double tau = 0.0, taun = 0.0;
     auto reflector = [&](const double (&x)[NT], int b, double (&v)[NT], double& t) {
-        double sig = 0.0;
+        double sq[NT];
 #pragma unroll
         for (int s = 0; s < NT; ++s) {
             const int j = lane + 32 * s;
-            if (j > b && j < n) sig += x[s] * x[s];
+            sq[s] = (j > b && j < n) ? x[s] * x[s] : 0.0;
         }
+        double sig = tree_sum<NT>(sq);  // pairwise within the lane: a 3-deep chain instead of NT
         sig = warp_sum_d(sig);
         const double alpha = vget<NT>(x, b);
         double beta = alpha;
         t = 0.0;
+        double scale = 0.0;
         if (sig > 0.0) {
-            const double nrm = sqrt(alpha * alpha + sig);
+            // one square root and one division: with beta = -sign(alpha) nrm, tau = (beta - alpha) / beta
+            // = 1 + |alpha| / nrm and 1 / (alpha - beta) = sign(alpha) / (|alpha| + nrm)
+            const double s2 = alpha * alpha + sig;
+            const double rn = rsqrt_fast(s2);  // 1 / nrm
+            const double nrm = s2 * rn;
+            const double aa = fabs(alpha);
             beta = alpha >= 0.0 ? -nrm : nrm;
-            t = (beta - alpha) / beta;
+            t = 1.0 + aa * rn;
+            scale = (alpha >= 0.0 ? 1.0 : -1.0) * rcp_fast(aa + nrm);
         }
-        const double scale = (sig > 0.0) ? 1.0 / (alpha - beta) : 0.0;
 #pragma unroll
         for (int s = 0; s < NT; ++s) {
             const int j = lane + 32 * s;
@@ -481,14 +518,16 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
         }
         return beta;
     };
+    // the reflector's global copy: slot s written by warp s % kT2Warps of CTA 0 (one store per lane and warp, so no
+    // warp carries the writes on the step's critical path)
     auto write_refl = [&](int k, const double (&v)[NT], double beta, double t) {
-        if (!writer) return;
+        if (q != 0) return;
 #pragma unroll
         for (int s = 0; s < NT; ++s) {
             const int j = lane + 32 * s;
-            if (j > k && j < n) ed.refl[(long long)k * n + (j - k - 1)] = v[s];
+            if (s % kT2Warps == warp && j > k && j < n) ed.refl[(long long)k * n + (j - k - 1)] = v[s];
         }
-        if (lane == 0) {
+        if (warp == kT2Warps - 1 && lane == 0) {
             ed.evec[k] = beta;
             ed.tau[k] = t;
         }
@@ -524,16 +563,16 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
         const double2* cur = pc + (k & 1) * n;
         TRC_PHASE(k, 8);
         // w_k = p_k - (tau_k / 2)(p_k . v_k) v_k
-        double P[NT];
-        double pv = 0.0;
+        double P[NT], pvs[NT];
 #pragma unroll
         for (int s = 0; s < NT; ++s) {
             const int j = lane + 32 * s;
             P[s] = (j >= b && j < n) ? cur[j].x : 0.0;
-            pv += P[s] * V[s];
+            pvs[s] = P[s] * V[s];
         }
-        pv = warp_sum_d(pv);
+        double pv = warp_sum_d(tree_sum<NT>(pvs));
         const double alpha2 = -0.5 * tau * pv;
+        TRC_PHASE(k, 12);
 #pragma unroll
         for (int s = 0; s < NT; ++s) W[s] = P[s] + alpha2 * V[s];
         // column b+... : x = column b after update k (entries j >= b; j = b is the diagonal d_b)
@@ -544,13 +583,15 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
             const int j = lane + 32 * s;
             x[s] = (j >= b && j < n) ? rank2(cur[j].y, V[s], wb, W[s], vb) : 0.0;
         }
+        TRC_PHASE(k, 13);
         const bool more = k + 3 < n;  // reflector b exists
-        if (writer) {
+        if (q == 0 && warp == kT2Warps - 2) {
             const double db = vget<NT>(x, b);
             if (lane == 0) ed.dvec[b] = db;
         }
         if (more) {
             const double beta = reflector(x, b + 1, Vn, taun);
+            TRC_PHASE(k, 14);
             write_refl(b, Vn, beta, taun);
         } else {
             // last 2 x 2: d_{n-1} comes from the pushed diagonal after this update; e_{n-2} = x_{n-1}
@@ -598,14 +639,16 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
                     for (int u = 0; u < U; ++u) a[u][s] = (ok[u] && j >= b + 1 && j < n) ? row[u][j] : 0.0;
                 }
 #pragma unroll
-                for (int s = 0; s < NT; ++s) {
-                    const int j = lane + 32 * s;
+                for (int u = 0; u < U; ++u) {
+                    double pr[NT];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                    for (int s = 0; s < NT; ++s) {
+                        const int j = lane + 32 * s;
                         a[u][s] = rank2(a[u][s], vi[u], W[s], wi[u], V[s]);
-                        dot[u] += a[u][s] * Vn[s];  // Vn is zero outside [b + 1, n)
+                        pr[s] = a[u][s] * Vn[s];  // Vn is zero outside [b + 1, n)
                         if (j == b + 1) cn[u] = a[u][s];
                     }
+                    dot[u] = tree_sum<NT>(pr);
                 }
 #pragma unroll
                 for (int s = 0; s < NT; ++s) {

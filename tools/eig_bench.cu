@@ -60,7 +60,8 @@ int main(int argc, char** argv) {
 #ifdef RKFAC_TRC_TIMING
     long long t[16];
     cudaMemcpyFromSymbol(t, g_trc, sizeof(t));
-    printf("one-barrier step %d: vectors %lld, pass %lld, barrier %lld cycles\n", RKFAC_TRC_TIMING, t[9] - t[8],
+    printf("one-barrier step %d: vectors %lld (pv %lld, x %lld, reflector %lld, write %lld), pass %lld, barrier %lld "
+           "cycles\n", RKFAC_TRC_TIMING, t[9] - t[8], t[12] - t[8], t[13] - t[12], t[14] - t[13], t[9] - t[14],
            t[10] - t[9], t[11] - t[10]);
     printf("step %d: reflector %lld, B %lld, sync1 %lld, C %lld, sync2 %lld cycles\n", RKFAC_TRC_TIMING, t[1] - t[0],
            t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
