@@ -433,7 +433,9 @@ constexpr int kT2Warps = kT2Threads / 32;
 
 size_t tridiag1b_smem_bytes(int n) {
     const int nloc = (n + kTcC - 1) / kTcC;
-    return ((((size_t)nloc * n + 1) & ~(size_t)1) + 4 * (size_t)n) * sizeof(double);
+    const int nt = n <= 256 ? 8 : 10;  // the kernel's NT
+    const int rmax = (32 * nt / kTcC + kT2Warps - 1) / kT2Warps;  // per-warp row partials of the deferred reduction
+    return ((((size_t)nloc * n + 1) & ~(size_t)1) + 4 * (size_t)n + (size_t)kT2Warps * rmax * 34) * sizeof(double);
 }
 
 template <int NT, int U>
@@ -451,6 +453,9 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
     double* R = tsm;                                                       // nloc x n
     double2* pc = reinterpret_cast<double2*>(R + (((size_t)((n + kTcC - 1) / kTcC) * n + 1) & ~(size_t)1));
     // pc: [2][n] of (p_i, A_{i,next column}), pushed by the row owners
+    constexpr int kRowsPerWarp = (32 * NT / kTcC + kT2Warps - 1) / kT2Warps;  // owned rows per warp, at most
+    double* wpart = reinterpret_cast<double*>(pc + 2 * n) + warp * (kRowsPerWarp * 33 + kRowsPerWarp);
+    double* wcn = wpart + kRowsPerWarp * 33;
     auto push = [&](int buf, int i, double p, double c) {  // lanes 0..3 store into CTA `lane`
         if (lane < kTcC) cluster.map_shared_rank(pc, lane)[buf * n + i] = make_double2(p, c);
     };
@@ -674,16 +679,40 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
                     }
                 }
 #endif
+                if constexpr (U == 1) {
+                    // deferred: the lane partials of every row go to shared memory and are summed after the loop,
+                    // all rows at once (one short transposed reduction instead of a 5-level butterfly per row)
+                    const int rr = (l0 - li_first - warp) / kT2Warps;
+                    wpart[rr * 33 + lane] = dot[0];
+                    if (((b + 1) & 31) == lane) wcn[rr] = cn[0];
+                } else {
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1)
+                    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-                    for (int u = 0; u < U; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+                        for (int u = 0; u < U; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int li = l0 + u * kT2Warps;
-                    const double c = __shfl_sync(0xffffffffu, cn[u], (b + 1) & 31);
-                    if (li < nloc) push((k + 1) & 1, q + kTcC * li, taun * dot[u], c);
+                    for (int u = 0; u < U; ++u) {
+                        const int li = l0 + u * kT2Warps;
+                        const double c = __shfl_sync(0xffffffffu, cn[u], (b + 1) & 31);
+                        if (li < nloc) push((k + 1) & 1, q + kTcC * li, taun * dot[u], c);
+                    }
                 }
+            }
+            if constexpr (U == 1) {
+                __syncwarp();
+                const int nrows = nloc > li_first + warp ? (nloc - li_first - warp + kT2Warps - 1) / kT2Warps : 0;
+                if (lane < nrows) {
+                    const double* pr = wpart + lane * 33;
+                    double t8[8];
+#pragma unroll
+                    for (int a8 = 0; a8 < 8; ++a8) t8[a8] = (pr[a8] + pr[a8 + 8]) + (pr[a8 + 16] + pr[a8 + 24]);
+                    const double dsum = tree_sum<8>(t8);
+                    const int i = q + kTcC * (li_first + warp + lane * kT2Warps);
+                    const double2 val = make_double2(taun * dsum, wcn[lane]);
+#pragma unroll
+                    for (int r = 0; r < kTcC; ++r) cluster.map_shared_rank(pc, r)[((k + 1) & 1) * n + i] = val;
+                }
+                __syncwarp();
             }
         }
         TRC_PHASE(k, 10);
