@@ -435,7 +435,8 @@ size_t tridiag1b_smem_bytes(int n) {
     const int nloc = (n + kTcC - 1) / kTcC;
     const int nt = n <= 256 ? 8 : 10;  // the kernel's NT
     const int rmax = (32 * nt / kTcC + kT2Warps - 1) / kT2Warps;  // per-warp row partials of the deferred reduction
-    return ((((size_t)nloc * n + 1) & ~(size_t)1) + 4 * (size_t)n + (size_t)kT2Warps * rmax * 34) * sizeof(double);
+    return ((((size_t)nloc * n + 1) & ~(size_t)1) + 4 * (size_t)n + (size_t)kT2Warps * rmax * 34 +
+            (size_t)kT2Warps * 64 * nt) * sizeof(double);
 }
 
 template <int NT, int U>
@@ -456,6 +457,9 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
     constexpr int kRowsPerWarp = (32 * NT / kTcC + kT2Warps - 1) / kT2Warps;  // owned rows per warp, at most
     double* wpart = reinterpret_cast<double*>(pc + 2 * n) + warp * (kRowsPerWarp * 33 + kRowsPerWarp);
     double* wcn = wpart + kRowsPerWarp * 33;
+    // per-warp copy of v_k and w_k (the pass reads v_i, w_i of each owned row with one broadcast load each)
+    double* sV = reinterpret_cast<double*>(pc + 2 * n) + kT2Warps * (kRowsPerWarp * 33 + kRowsPerWarp) + warp * 64 * NT;
+    double* sW = sV + 32 * NT;
     auto push = [&](int buf, int i, double p, double c) {  // lanes 0..3 store into CTA `lane`
         if (lane < kTcC) cluster.map_shared_rank(pc, lane)[buf * n + i] = make_double2(p, c);
     };
@@ -579,7 +583,12 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
         const double alpha2 = -0.5 * tau * pv;
         TRC_PHASE(k, 12);
 #pragma unroll
-        for (int s = 0; s < NT; ++s) W[s] = P[s] + alpha2 * V[s];
+        for (int s = 0; s < NT; ++s) {
+            W[s] = P[s] + alpha2 * V[s];
+            sV[lane + 32 * s] = V[s];
+            sW[lane + 32 * s] = W[s];
+        }
+        __syncwarp();
         // column b+... : x = column b after update k (entries j >= b; j = b is the diagonal d_b)
         const double vb = vget<NT>(V, b), wb = vget<NT>(W, b);
         double x[NT];
@@ -627,8 +636,8 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
                     ok[u] = l0 + u * kT2Warps < nloc;
                     const int li = min(l0 + u * kT2Warps, nloc - 1);
                     const int i = q + kTcC * li;
-                    vi[u] = vget<NT>(V, i);
-                    wi[u] = vget<NT>(W, i);
+                    vi[u] = sV[i];
+                    wi[u] = sW[i];
                     dot[u] = 0.0;
                     cn[u] = 0.0;
                     row[u] = R + (size_t)li * n;
