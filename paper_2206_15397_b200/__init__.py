@@ -608,6 +608,7 @@ class StreamedStep:
                 if pri[g] > lo_pri:
                     pri[g] = lo_pri
         self.streams = [torch.cuda.Stream(device=device, priority=pri[g]) for g in range(len(self.subs))]
+        self._issue_order = order
         # views in the original order
         self.dims, self.factors, self.samples, self.bases_t, self.dvals, self.ranks = [], [], [], [], [], []
         self.grads, self.outs, self.mids = [None] * nl, [None] * nl, [None] * nl
@@ -681,7 +682,8 @@ class StreamedStep:
         fork = torch.cuda.Event()
         fork.record(main)
         joins = []
-        for sub, st, cp, part in zip(self.subs, self.streams, self._copy_streams, self.parts):
+        for g in self._issue_order:  # the critical group's uploads first
+            sub, st, cp, part = self.subs[g], self.streams[g], self._copy_streams[g], self.parts[g]
             st.wait_event(fork)
             with torch.cuda.stream(st):
                 for i, l in enumerate(part):

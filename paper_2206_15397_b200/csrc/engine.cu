@@ -56,8 +56,10 @@ TcOut out_t(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 1; retu
 // 1.4e-5, orthonormality 1.1e-4 -> 7.8e-6.
 constexpr int kSliceK = 512;
 constexpr int kSliceKFinal = 1024;
-// the apply's long-K products write d_G x r partials per slice (1 GB per layer at d = 16384 with 512-slices)
-constexpr int kSliceKApply = 2048;
+// The apply's long-K products: at most 8 slices of at least 512 (a slice is one TMEM chain: its length is the
+// latency of the product -- 2048-long slices put ~100 us on a VGG16 group's critical path -- while more slices write
+// more d_G x r partials: 1 GB per layer at d = 16384 with 512-slices)
+static int apply_slice(int K) { return std::max(512, (K + 7) / 8); }
 
 TcOut out_r(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 0; return o; }
 
@@ -503,7 +505,7 @@ void Plan::build_apply_stages(double lambda) {
         p0.B = A.Uti; p0.B_lo = A.Utilo; p0.ldb = A.dp;
         p0.cs = A.bracket;
         p0.out0 = out_r(L.W1, A.rp); p0.lo0 = out_r(L.W1lo, A.rp);
-        p0.slice_k = kSliceKApply;
+        p0.slice_k = apply_slice(A.d);
         ap_[0]->add(p0);
         TcProblemDesc p1;
         p1.M = G.d; p1.N = A.d; p1.K = A.r;
@@ -518,7 +520,7 @@ void Plan::build_apply_stages(double lambda) {
         p2.B = L.Mt; p2.B_lo = L.Mtlo; p2.ldb = dGp;
         p2.rs = G.bracket;
         p2.out0 = out_t(L.W2t, G.rp); p2.lo0 = out_t(L.W2tlo, G.rp);
-        p2.slice_k = kSliceKApply;
+        p2.slice_k = apply_slice(G.d);
         ap_[2]->add(p2);
         TcProblemDesc p3;
         p3.M = G.d; p3.N = A.d; p3.K = G.r;
