@@ -216,3 +216,79 @@ class KfacOptimizer:
         self.timings.decomposition += ev[0].elapsed_time(ev[1]) / 1e3
         self.timings.inverse_apply += ev[1].elapsed_time(ev[2]) / 1e3
         return outs
+
+
+# ------------------------------------------------------------------ spectrum snapshots and run logs (8(f) #4)
+@dataclass
+class SpectrumReport:  # kfactor.hpp:44-54
+    eigenvalues: list          # decreasing, clamped at 0
+    lambda_max: float = 0.0
+
+    def count_above(self, epsilon: float) -> int:
+        thr = epsilon * self.lambda_max
+        return sum(1 for v in self.eigenvalues if v >= thr)
+
+
+def spectrum(factor) -> SpectrumReport:
+    """kfactor.hpp:56-63 on a device factor: full eigenvalues (FP64 eigensolve of the FP32 factor), clamped at 0."""
+    from . import sym_eig
+
+    d = sym_eig(factor.contiguous(), fp64=True).d.double().cpu().tolist()
+    ev = [max(0.0, v) for v in d]
+    return SpectrumReport(ev, ev[0] if ev else 0.0)
+
+
+@dataclass
+class SpectrumSnapshot:  # harness.hpp:65-69
+    step: int
+    layer: int
+    eigenvalues: list
+
+
+@dataclass
+class StepRecord:  # harness.hpp (run log row)
+    step: int
+    epoch: int
+    loss: float
+    acc: float
+    timings: StepTimings
+
+
+def snapshot_a_factors(opt: "KfacOptimizer", step: int) -> List[SpectrumSnapshot]:
+    """harness.hpp:214-218: the forward (A) factor spectrum of every layer."""
+    return [SpectrumSnapshot(step, l, spectrum(opt.plan.factors[2 * l]).eigenvalues) for l in range(len(opt.layers))]
+
+
+def _fmt(v: float) -> str:  # harness.hpp:239-243 ("%.17g")
+    return "%.17g" % v
+
+
+def write_runlog_csv(path: str, steps: Sequence[StepRecord]):
+    """harness.hpp:276-285: step,epoch,loss,acc,t_factor,t_decomp,t_apply."""
+    with open(path, "w") as f:
+        f.write("step,epoch,loss,acc,t_factor,t_decomp,t_apply\n")
+        for r in steps:
+            f.write(f"{r.step},{r.epoch},{_fmt(r.loss)},{_fmt(r.acc)},{_fmt(r.timings.factor_update)},"
+                    f"{_fmt(r.timings.decomposition)},{_fmt(r.timings.inverse_apply)}\n")
+
+
+def write_spectrum_csv(path: str, snapshots: Sequence[SpectrumSnapshot]):
+    """harness.hpp:287-293: step,layer,idx,eigenvalue."""
+    with open(path, "w") as f:
+        f.write("step,layer,idx,eigenvalue\n")
+        for s in snapshots:
+            for i, v in enumerate(s.eigenvalues):
+                f.write(f"{s.step},{s.layer},{i},{_fmt(v)}\n")
+
+
+def decay_orders(eigenvalues: Sequence[float], modes: int) -> float:
+    """harness.hpp:307-315: log10(lambda_1 / lambda_m) over the first `modes` eigenvalues."""
+    if not eigenvalues:
+        return 0.0
+    m = min(modes, len(eigenvalues))
+    head, tail = eigenvalues[0], eigenvalues[m - 1]
+    if head <= 0.0:
+        return 0.0
+    if tail <= 0.0:
+        return 300.0
+    return math.log10(head / tail)

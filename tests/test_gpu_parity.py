@@ -506,3 +506,15 @@ def test_kfac_optimizer_cache_and_schedule_match_oracle(port, cuda, method):
                 s0 = port.precondition(ua, da, ug, dg, lam, grads[l])
             assert rel_fro(np64(outs[l]), s0) < TOL, (k, l)
     assert opt.timings.decomposition > 0 and opt.timings.inverse_apply > 0
+
+
+def test_spectrum_snapshot_matches_oracle(port, cuda):
+    """kfactor.hpp:56-63 spectrum on the device factor vs the oracle's sym_eig (clamped at 0)."""
+    from paper_2206_15397_b200.kfac import spectrum
+
+    x = build_factor(port, 200, 64, 5, 1.0, f=0)
+    _, d0 = port.sym_eig(x)
+    rep = spectrum(t32(x, cuda))
+    ev = np.asarray(rep.eigenvalues)
+    top = np.maximum(d0, 0.0)[:40]
+    assert eig_err(ev[:40], top) < TOL and rep.lambda_max == pytest.approx(top[0], rel=1e-6)

@@ -54,3 +54,19 @@ def test_factor_statistics_appends_the_ones_row():
     assert am[0].shape == (6, 8) and torch.equal(am[0][:5], a) and torch.equal(am[0][5], torch.ones(8))
     assert gm[0] is d
     assert Method.SRE_KFAC.value == 2
+
+
+def test_runlog_and_spectrum_csv_schema(tmp_path):
+    from paper_2206_15397_b200.kfac import (SpectrumReport, SpectrumSnapshot, StepRecord, StepTimings, decay_orders,
+                                            write_runlog_csv, write_spectrum_csv)
+
+    write_runlog_csv(str(tmp_path / "runlog.csv"), [StepRecord(0, 0, 2.5, -1.0, StepTimings(0.1, 0.2, 0.3))])
+    assert (tmp_path / "runlog.csv").read_text().splitlines() == [
+        "step,epoch,loss,acc,t_factor,t_decomp,t_apply", "0,0,2.5,-1,0.10000000000000001,0.20000000000000001,"
+        "0.29999999999999999"]
+    write_spectrum_csv(str(tmp_path / "spectrum.csv"), [SpectrumSnapshot(3, 1, [2.0, 0.5])])
+    assert (tmp_path / "spectrum.csv").read_text().splitlines() == ["step,layer,idx,eigenvalue", "3,1,0,2", "3,1,1,0.5"]
+    assert decay_orders([100.0, 10.0, 1.0], 3) == pytest.approx(2.0)
+    assert decay_orders([1.0, 0.0], 2) == 300.0 and decay_orders([], 5) == 0.0
+    rep = SpectrumReport([4.0, 2.0, 0.5, 0.0], 4.0)
+    assert rep.count_above(0.1) == 3
