@@ -590,7 +590,7 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
         }
         __syncwarp();
         // column b+... : x = column b after update k (entries j >= b; j = b is the diagonal d_b)
-        const double vb = vget<NT>(V, b), wb = vget<NT>(W, b);
+        const double vb = sV[b], wb = sW[b];  // the per-warp copy written just above
         double x[NT];
 #pragma unroll
         for (int s = 0; s < NT; ++s) {
