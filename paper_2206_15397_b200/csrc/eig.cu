@@ -1312,43 +1312,24 @@ __global__ void __launch_bounds__(kWyThreads) backxform_wy_kernel(const EigDesc*
         }
         __syncthreads();
         BX_PHASE(b, 2);
-        // T = (diag(1/tau) + striu(V^T V))^{-1} (compact WY, forward columnwise): lane j back-substitutes column j,
-        // T(i, j) = -tau_i sum_{l=i+1}^{j} G(i, l) T(l, j), T(j, j) = tau_j (tau_i = 0 gives a zero row and column)
-        if (warp == 0) {
-            double t[kWyB];
-            const int j = lane;
+        // W <- T W with T = (diag(1/tau) + striu(V^T V))^{-1} (compact WY, forward columnwise), as one triangular
+        // solve (diag(1/tau) + striu(G)) X = W: a thread per eigenvector column back-substitutes, x_i =
+        // tau_i (w_i - sum_{l>i} G(i, l) x_l), right-looking (after x_i, every w_l, l < i, loses G(l, i) x_i), so
+        // neither T nor the T W product is formed (tau_i = 0 gives x_i = 0: the identity reflector)
+        BX_PHASE(b, 3);
+        if (tid < kWyC) {
+            const int c = tid;
+            double x[kWyB];
+#pragma unroll
+            for (int i = 0; i < kWyB; ++i) x[i] = W[i * kWyWP + c];
 #pragma unroll
             for (int i = kWyB - 1; i >= 0; --i) {
-                double acc = 0.0;
+                x[i] *= taus[i];
 #pragma unroll
-                for (int l = i + 1; l < kWyB; ++l) acc += G[i * kWyP + l] * t[l];  // t[l] = 0 for l > j
-                t[i] = (i > j) ? 0.0 : (i == j ? taus[j] : -taus[i] * acc);
+                for (int l = 0; l < i; ++l) x[l] -= G[l * kWyP + i] * x[i];
             }
 #pragma unroll
-            for (int i = 0; i < kWyB; ++i) T[i * kWyP + j] = t[i];
-        }
-        __syncthreads();
-        BX_PHASE(b, 3);
-        // W <- T W (T upper triangular; the stored zeros are summed), in registers then back
-        double tw[2][kWyB / kWyWarps];
-#pragma unroll
-        for (int u = 0; u < kWyB / kWyWarps; ++u) {
-            const int j = warp + u * kWyWarps;
-            double a0 = 0.0, a1 = 0.0;
-#pragma unroll 8
-            for (int l = 0; l < kWyB; ++l) {
-                const double t = T[j * kWyP + l];
-                a0 += t * W[l * kWyWP + lane];
-                a1 += t * W[l * kWyWP + lane + 32];
-            }
-            tw[0][u] = a0;
-            tw[1][u] = a1;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kWyB / kWyWarps; ++u) {
-            W[(warp + u * kWyWarps) * kWyWP + lane] = tw[0][u];
-            W[(warp + u * kWyWarps) * kWyWP + lane + 32] = tw[1][u];
+            for (int i = 0; i < kWyB; ++i) W[i * kWyWP + c] = x[i];
         }
         __syncthreads();
         BX_PHASE(b, 4);
