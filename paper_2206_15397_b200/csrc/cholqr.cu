@@ -576,7 +576,13 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
 // Two cluster barriers per 32 columns (16 for w = 230) instead of the single CTA's serial TRSM and log-depth
 // inversion; every product has a fixed order (deterministic).
 constexpr int kCC = 4;
-constexpr int kCcThreads = 384;
+#ifndef RKFAC_CC_THREADS
+#define RKFAC_CC_THREADS 256  // 192 / 256 / 384 / 512 measured: 256 best (FP32 113 us, FP64 193 us at w = 230)
+#endif
+#ifndef RKFAC_CC_DEFER64
+#define RKFAC_CC_DEFER64 0
+#endif
+constexpr int kCcThreads = RKFAC_CC_THREADS;
 constexpr int kCcMaxBlk = 16;
 
 __host__ __device__ __forceinline__ int cc_owner(int b) {
@@ -748,7 +754,7 @@ __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
                     for (int j = k + 1; j < kNB; ++j) a[j] -= a[k - 1] * tp[j];
                 }
             };
-            constexpr bool kDefer = sizeof(T) == 4;
+            constexpr bool kDefer = sizeof(T) == 4 || RKFAC_CC_DEFER64;
             if (nb == kNB) {
 #pragma unroll
                 for (int k = 0; k < kNB; ++k) step(k, kNB, kDefer);
