@@ -309,6 +309,7 @@ void Plan::build_decomp_stages() {
         xqf_[dir] = new_tc();
         gram_[dir] = new_tc();
         tri_[dir] = new_tc();
+        tri_t_[dir] = new_tc();
         core_[dir] = new_tc();
         gram64_[dir] = std::make_unique<Gram64Batch>();
         tri64_[dir] = std::make_unique<Tri64Batch>();
@@ -349,6 +350,7 @@ void Plan::build_decomp_stages() {
                 t.A = Y.R; t.A_lo = Y.Rlo; t.lda = F.wp;
                 t.B = F.Linv32; t.B_lo = F.Linv32lo; t.ldb = F.wp;
                 t.out0 = out_t(Q.T, F.dp); t.lo0 = out_t(Q.Tlo, F.dp);
+                tri_t_[dir]->add(t);  // intermediate bases: only the X*Q operand planes (Q^T and its lo plane)
                 t.out1 = out_r(Q.R, F.wp); t.lo1 = out_r(Q.Rlo, F.wp);
                 tri_[dir]->add(t);
             }
@@ -388,7 +390,7 @@ void Plan::build_decomp_stages() {
             return !(e && e[0] == '0');
         }();
         gram_[dir]->set_defer_reduce(fuse_gram);  // the Cholesky-inverse sums the Gram's K slices while loading it
-        xq_[dir]->finalize(); xqf_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); core_[dir]->finalize();
+        xq_[dir]->finalize(); xqf_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); tri_t_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
     std::vector<CopyDesc> cp;
@@ -535,7 +537,7 @@ void Plan::build_apply_stages(double lambda) {
 }
 
 // Orthonormalise role S[src] into S[src ^ 1].
-void Plan::orth(int src, bool fp64, cudaStream_t s) {
+void Plan::orth(int src, bool fp64, cudaStream_t s, bool need_r) {
     const int n = nfactors();
     if (fp64) {
         gram64_[src]->launch(s);
@@ -544,7 +546,7 @@ void Plan::orth(int src, bool fp64, cudaStream_t s) {
     } else {
         gram_[src]->launch(s);
         launch_cholinv(d_chol32_[src].as<CholDesc>(), n, wmax_, false, false, kTol32, s);
-        tri_[src]->launch(s);
+        (need_r ? tri_ : tri_t_)[src]->launch(s);
     }
     // rank-deficient columns stay zero here; the final basis is completed in decompose()
 }
@@ -623,7 +625,8 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
         timed_xq(y, o);
         last_fp64 = o < n_fp64_orth_;
         mark(kOrth, true);
-        orth(y, last_fp64, s);  // S[y] -> S[cur_q]
+        // S[y] -> S[cur_q]; the row-major planes of Q are read only by the CholeskyQR2 pass and the lift
+        orth(y, last_fp64, s, o == north - 1);
         mark(kOrth, false);
     }
     if (!last_fp64) {  // CholeskyQR2: second pass so the final basis is orthonormal to FP32 rounding
