@@ -307,6 +307,7 @@ void Plan::build_decomp_stages() {
     for (int dir = 0; dir < 2; ++dir) {
         xq_[dir] = new_tc();
         xqf_[dir] = new_tc();
+        xq_t_[dir] = new_tc();
         gram_[dir] = new_tc();
         tri_[dir] = new_tc();
         tri_t_[dir] = new_tc();
@@ -332,7 +333,13 @@ void Plan::build_decomp_stages() {
                 // (N tiles of 128 instead of one 240-column tile: measured 46 % slower; splitting only the d >= 4096
                 // factors' K in two: X*Q stage 3.28 -> 4.18 ms)
                 xq_[dir]->add(p);
+                // the products whose Y planes feed only T-plane consumers: before an FP64 orthonormalisation (its Gram
+                // and Y L^-T read Y^T) and, for srevd, the final product (the core reads Y^T; the lift reads Q)
+                TcProblemDesc pt = p;
+                pt.out1 = TcOut{}; pt.lo1 = TcOut{};
+                xq_t_[dir]->add(pt);
                 p.slice_k = kSliceKFinal;
+                if (method_ == RKFAC_SREVD) { p.out1 = TcOut{}; p.lo1 = TcOut{}; }
                 xqf_[dir]->add(p);
 
             }
@@ -390,7 +397,7 @@ void Plan::build_decomp_stages() {
             return !(e && e[0] == '0');
         }();
         gram_[dir]->set_defer_reduce(fuse_gram);  // the Cholesky-inverse sums the Gram's K slices while loading it
-        xq_[dir]->finalize(); xqf_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); tri_t_[dir]->finalize(); core_[dir]->finalize();
+        xq_[dir]->finalize(); xqf_[dir]->finalize(); xq_t_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); tri_t_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
     std::vector<CopyDesc> cp;
@@ -613,9 +620,9 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     // Every power product runs in 3xTF32: 1xTF32 intermediate products (0.7 ms faster per VGG16 step) were measured
     // to move the poorly converged Ritz values near the cut-off by up to 6e-3 (d = 16384) -- first order in the
     // perturbation of the subspace -- so the reference's randomized answer is not reproduced to 1e-4.
-    auto timed_xq = [&](int y, int) {
+    auto timed_xq = [&](int y, int o) {
         mark(kXQ, true);
-        xq_[y]->launch(s);
+        (o < n_fp64_orth_ ? xq_t_ : xq_)[y]->launch(s);  // an FP64 orthonormalisation reads only Y^T
         mark(kXQ, false);
     };
     // Every product is orthonormalised, as in the reference: skipping alternate orthonormalisations (X X Q, same

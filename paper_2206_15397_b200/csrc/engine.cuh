@@ -135,7 +135,7 @@ class Plan {
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
     // xqf_: the final X*Q (input of the core) with short accumulation chains (see kSliceK in engine.cu)
-    std::unique_ptr<TcGemm> xq_[2], xqf_[2], gram_[2], tri_[2], tri_t_[2], core_[2], lift_[2];
+    std::unique_ptr<TcGemm> xq_[2], xq_t_[2], xqf_[2], gram_[2], tri_[2], tri_t_[2], core_[2], lift_[2];
     std::unique_ptr<Gram64Batch> gram64_[2];
     std::unique_ptr<Tri64Batch> tri64_[2];
     std::unique_ptr<TcGemm> ea_tc_stage_;
