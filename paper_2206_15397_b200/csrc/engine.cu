@@ -320,14 +320,16 @@ void Plan::build_decomp_stages() {
             Role& Y = F.S[dir];      // written by xq_[dir]; source of the orthonormalisation indexed dir
             Role& Q = F.S[dir ^ 1];  // basis read by xq_[dir]; destination of orth(src = dir)
             const float* Xop = x_tma_ok_ ? F.X : F.Xc;
-            // Y = X Q (all four planes of Y):  A = X (d x d), B = Q^T (w x d)
+            // Y = X Q (Y^T with its TF32 lo plane for the Gram and the core; Y row-major without: the Y L^-T and lift
+            // products form that lo plane in smem -- measured: forming Y^T's lo plane in the Gram too is slower):
+            // A = X (d x d), B = Q^T (w x d)
             {
                 TcProblemDesc p;
                 p.M = F.d; p.N = F.w; p.K = F.d;
                 p.A = Xop; p.A_lo = nullptr; p.lda = F.ldxa;  // X's lo plane is formed in shared memory
                 p.B = Q.T; p.B_lo = Q.Tlo; p.ldb = F.dp;
                 p.out0 = out_t(Y.T, F.dp); p.lo0 = out_t(Y.Tlo, F.dp);
-                p.out1 = out_r(Y.R, F.wp); p.lo1 = out_r(Y.Rlo, F.wp);
+                p.out1 = out_r(Y.R, F.wp);
                 // unsplit: K slices of 1-2K for the power products were measured 30-40 % slower (partials + the
                 // 4-output reduction) without shortening the step
                 // (N tiles of 128 instead of one 240-column tile: measured 46 % slower; splitting only the d >= 4096
@@ -336,10 +338,10 @@ void Plan::build_decomp_stages() {
                 // the products whose Y planes feed only T-plane consumers: before an FP64 orthonormalisation (its Gram
                 // and Y L^-T read Y^T) and, for srevd, the final product (the core reads Y^T; the lift reads Q)
                 TcProblemDesc pt = p;
-                pt.out1 = TcOut{}; pt.lo1 = TcOut{};
+                pt.out1 = TcOut{};
                 xq_t_[dir]->add(pt);
                 p.slice_k = kSliceKFinal;
-                if (method_ == RKFAC_SREVD) { p.out1 = TcOut{}; p.lo1 = TcOut{}; }
+                if (method_ == RKFAC_SREVD) p.out1 = TcOut{};
                 xqf_[dir]->add(p);
 
             }
@@ -354,11 +356,11 @@ void Plan::build_decomp_stages() {
                 gram_[dir]->add(g);
                 TcProblemDesc t;
                 t.M = F.d; t.N = F.w; t.K = F.w;
-                t.A = Y.R; t.A_lo = Y.Rlo; t.lda = F.wp;
+                t.A = Y.R; t.A_lo = nullptr; t.lda = F.wp;
                 t.B = F.Linv32; t.B_lo = F.Linv32lo; t.ldb = F.wp;
                 t.out0 = out_t(Q.T, F.dp); t.lo0 = out_t(Q.Tlo, F.dp);
                 tri_t_[dir]->add(t);  // intermediate bases: only the X*Q operand planes (Q^T and its lo plane)
-                t.out1 = out_r(Q.R, F.wp); t.lo1 = out_r(Q.Rlo, F.wp);
+                t.out1 = out_r(Q.R, F.wp);
                 tri_[dir]->add(t);
             }
             // FP64 CholeskyQR of Y into Q (DMMA): G = Y^T Y in FP64, Q^T = Linv Y^T with FP64 accumulation
@@ -382,7 +384,7 @@ void Plan::build_decomp_stages() {
                 TcProblemDesc lf;
                 lf.M = F.d; lf.N = F.r; lf.K = F.w;
                 const Role& Aop = method_ == RKFAC_SREVD ? Q : Y;
-                lf.A = Aop.R; lf.A_lo = Aop.Rlo; lf.lda = F.wp;
+                lf.A = Aop.R; lf.A_lo = nullptr; lf.lda = F.wp;
                 lf.B = F.Pt; lf.B_lo = F.Ptlo; lf.ldb = F.wp;
                 if (method_ == RKFAC_RSVD) lf.cs = F.scale;
                 lf.out0 = out_t(F.Uti, F.dp); lf.lo0 = out_t(F.Utilo, F.dp);
