@@ -688,12 +688,16 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
                     }
                 }
 #endif
-                if constexpr (U == 1) {
+                if constexpr (true) {
                     // deferred: the lane partials of every row go to shared memory and are summed after the loop,
                     // all rows at once (one short transposed reduction instead of a 5-level butterfly per row)
                     const int rr = (l0 - li_first - warp) / kT2Warps;
-                    wpart[rr * 33 + lane] = dot[0];
-                    if (((b + 1) & 31) == lane) wcn[rr] = cn[0];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (ok[u]) {
+                            wpart[(rr + u) * 33 + lane] = dot[u];
+                            if (((b + 1) & 31) == lane) wcn[rr + u] = cn[u];
+                        }
                 } else {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1)
@@ -707,7 +711,7 @@ __global__ void __cluster_dims__(kTcC, 1, 1) __launch_bounds__(kT2Threads)
                     }
                 }
             }
-            if constexpr (U == 1) {
+            if constexpr (true) {
                 __syncwarp();
                 const int nrows = nloc > li_first + warp ? (nloc - li_first - warp + kT2Warps - 1) / kT2Warps : 0;
                 if (lane < nrows) {
