@@ -339,6 +339,7 @@ void Plan::build_decomp_stages() {
                 // and Y L^-T read Y^T) and, for srevd, the final product (the core reads Y^T; the lift reads Q)
                 TcProblemDesc pt = p;
                 pt.out1 = TcOut{};
+                pt.lo0 = TcOut{};  // the FP64 Gram and Y L^-T read Y^T itself (FP64 DMMA), not its TF32 lo plane
                 xq_t_[dir]->add(pt);
                 p.slice_k = kSliceKFinal;
                 if (method_ == RKFAC_SREVD) p.out1 = TcOut{};
