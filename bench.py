@@ -534,7 +534,7 @@ def main():
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--groups", type=int, default=4, help="layer groups on concurrent streams (StreamedStep)")
+    ap.add_argument("--groups", type=int, default=5, help="layer groups on concurrent streams (StreamedStep; 5 gave the best e2e)")
     ap.add_argument("--profile-step", action="store_true", help="run one step under cudaProfilerStart/Stop and exit")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
                     help="replay the timed step as one CUDA graph (rk.StepGraph); measured within 0.5 %% of eager")
