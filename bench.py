@@ -342,17 +342,21 @@ def run_ours(args, wl):
 
     graph = None  # CUDA graph of the whole step (rk.StepGraph), captured after the eager warm-up
 
+    def gather():
+        """The one collective: pack this rank's preconditioned gradients and all-gather them.  On one
+        GPU every layer's result is already in place, so there is nothing to move."""
+        if world == 1:
+            return
+        for i, l in enumerate(mine):
+            send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
+        dist.all_gather_into_tensor(recv, send)
+
     def one_step():
         if graph is not None:
             graph.replay()
         else:
             step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
-        for i, l in enumerate(mine):
-            send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
-        if world > 1:
-            dist.all_gather_into_tensor(recv, send)
-        else:
-            recv.copy_(send)
+        gather()
 
     def reset(st=None):
         for x, x0 in zip((st or step).factors, factors0):
@@ -428,24 +432,14 @@ def run_ours(args, wl):
             for hg, dg in zip(h_grads, step.grads):
                 dg.copy_(hg, non_blocking=True)
             step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
-            for i, l in enumerate(mine):
-                send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
-            if world > 1:
-                dist.all_gather_into_tensor(recv, send)
-            else:
-                recv.copy_(send)
+            gather()
             for ho, do in zip(h_outs, step.outs):
                 ho.copy_(do, non_blocking=True)
             return
         # the public host-buffer step: per group, samples H2D -> EA -> rand-EVD while the gradients upload on a copy
         # stream, then precondition -> results D2H (one group's copies overlap the other group's kernels)
         step.step_host(OMEGA_ROOT, 0, lam, h_samples, h_grads, h_outs, 0.95, 1.0)
-        for i, l in enumerate(mine):
-            send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
-        if world > 1:
-            dist.all_gather_into_tensor(recv, send)
-        else:
-            recv.copy_(send)
+        gather()
 
     for i in range(args.warmup + args.steps):
         reset()
@@ -494,7 +488,7 @@ def run_ours(args, wl):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "factors": nf_total, "layers": len(layers), "rank": r,
                        "oversampling": p, "power_iters": q, "lambda": lam, "n": n, "method": "srevd",
-                       "parallelism": f"layer-LPT x{world} + NCCL all-gather",
+                       "parallelism": f"layer-LPT x{world}" + (" + NCCL all-gather" if world > 1 else " (no collective on one GPU)"),
                        "streams_per_gpu": args.groups,
                        "l2": f"inputs ({sum(4 * d * d for a, g in layers for d in (a, g)) / 1e6:.0f} MB of factors) "
                              "exceed the 126 MB L2; no flush",
