@@ -493,7 +493,7 @@ def run_ours(args, wl):
                        "l2": f"inputs ({sum(4 * d * d for a, g in layers for d in (a, g)) / 1e6:.0f} MB of factors) "
                              "exceed the 126 MB L2; no flush",
                        "value_def": "factors inverted per second of the whole step (EA + rand-EVD + precondition "
-                                    "+ all-gather) = factors / step time"},
+                                    "+ the all-gather on N > 1 GPUs) = factors / step time"},
             "precond_step_ms": ms,
             "stage_ms": stages,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": xq_peak, "unit": "TFLOP/s",
