@@ -801,7 +801,10 @@ __device__ __forceinline__ int sturm_count_p(const double* __restrict__ d, const
     return sturm_count_impl<true>(d, e2, n, x, zero);
 }
 
-constexpr int kBisG = 4;    // threads per eigenvalue: 5-section per iteration
+#ifndef RKFAC_BIS_G
+#define RKFAC_BIS_G 4
+#endif
+constexpr int kBisG = RKFAC_BIS_G;  // threads per eigenvalue: (kBisG+1)-section per iteration
 constexpr int kBisE = 32;   // eigenvalues per CTA
 constexpr int kBisThreads = kBisG * kBisE;
 
