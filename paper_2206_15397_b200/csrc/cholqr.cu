@@ -575,7 +575,10 @@ __global__ void __launch_bounds__(kCholThreads) cholinv_kernel(const CholDesc* _
 //      trailing A_ic -= P_i . P_c (J0+32 <= c <= i) and inverse R_i(:, 0:J0+32) -= P_i X_b.
 // Two cluster barriers per 32 columns (16 for w = 230) instead of the single CTA's serial TRSM and log-depth
 // inversion; every product has a fixed order (deterministic).
-constexpr int kCC = 4;
+#ifndef RKFAC_CC_CTAS
+#define RKFAC_CC_CTAS 4  // CTAs per cluster (per factor)
+#endif
+constexpr int kCC = RKFAC_CC_CTAS;
 #ifndef RKFAC_CC_THREADS
 #define RKFAC_CC_THREADS 256  // 192 / 256 / 384 / 512 measured: 256 best (FP32 113 us, FP64 193 us at w = 230)
 #endif
