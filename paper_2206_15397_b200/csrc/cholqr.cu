@@ -585,6 +585,14 @@ constexpr int kCC = RKFAC_CC_CTAS;
 #ifndef RKFAC_CC_DEFER64
 #define RKFAC_CC_DEFER64 0
 #endif
+#ifndef RKFAC_CC_TW32
+// columns per register tile of the trailing / inverse update; 4 or 8. 8 measured slower (tools/chol_tw_sweep.sh,
+// w = 230: 122 vs 115 us FP32, 219 vs 195 us FP64): the update is latency-bound, fewer tiles leave threads idle
+#define RKFAC_CC_TW32 4
+#endif
+#ifndef RKFAC_CC_TW64
+#define RKFAC_CC_TW64 4
+#endif
 constexpr int kCcThreads = RKFAC_CC_THREADS;
 constexpr int kCcMaxBlk = 16;
 
@@ -907,12 +915,18 @@ __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
         // ------------------------------------------------ 3. trailing update and inverse update of the owned rows
         {
             // row groups of 4 owned rows below block b; group at row i0 has i0/4 + 1 column tiles (0 .. i0)
-            int total = 0;
-            for (int ob = b + 1; ob < nblk; ++ob) {
-                if (boff[ob] < 0) continue;
+            // tiles are 4 rows x kTW columns; group g of block ob covers columns 0 .. ob*kNB + 4g + 3
+            constexpr int kTW = sizeof(T) == 4 ? RKFAC_CC_TW32 : RKFAC_CC_TW64;
+            auto ntile = [&](int ob, int g) { return ob * (kNB / kTW) + (4 * g + 4 + kTW - 1) / kTW; };
+            auto ntiles_blk = [&](int ob) {
                 const int G4 = (min(kNB, n - ob * kNB) + 3) / 4;
-                total += G4 * (ob * 8 + 1) + G4 * (G4 - 1) / 2;
-            }
+                int t = 0;
+                for (int g = 0; g < G4; ++g) t += ntile(ob, g);
+                return t;
+            };
+            int total = 0;
+            for (int ob = b + 1; ob < nblk; ++ob)
+                if (boff[ob] >= 0) total += ntiles_blk(ob);
             const int jb = J0 + kNB;  // first trailing column
             // look-ahead: the owner of block b+1 updates that block's diagonal tiles first, then one warp factors it
             // while the others finish the update
@@ -921,17 +935,16 @@ __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
                 int rem = t, ob = b + 1, g = 0;
                 for (; ob < nblk; ++ob) {
                     if (boff[ob] < 0) continue;
-                    const int G4 = (min(kNB, n - ob * kNB) + 3) / 4;
-                    const int tiles = G4 * (ob * 8 + 1) + G4 * (G4 - 1) / 2;
+                    const int tiles = ntiles_blk(ob);
                     if (rem < tiles) break;
                     rem -= tiles;
                 }
                 for (;; ++g) {
-                    const int tg = ob * 8 + g + 1;
+                    const int tg = ntile(ob, g);
                     if (rem < tg) break;
                     rem -= tg;
                 }
-                obo = ob; go = g; c0o = rem * 4;
+                obo = ob; go = g; c0o = rem * kTW;
                 diag_next = ob == b + 1 && c0o >= jb;
             };
             auto run = [&](int ob, int g, int c0) {
@@ -941,34 +954,48 @@ __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kCcThreads)
                 const bool inv_tile = c0 < jb;
                 const T* bop = inv_tile ? (xb + c0) : (panel + c0);
                 const int bld = inv_tile ? xbp : np;
-                T acc[4][4] = {};
+                T acc[4][kTW] = {};
 #pragma unroll 8
                 for (int k = 0; k < kNB; ++k) {  // nb == kNB: every block but the last has a trailing update
-                    T av[4], bv[4];
+                    T av[4], bv[kTW];
                     ld4(panel + k * np + i0, av);
-                    ld4(bop + k * bld, bv);
+#pragma unroll
+                    for (int v4 = 0; v4 < kTW; v4 += 4) {
+                        T t4[4];
+                        ld4(bop + k * bld + v4, t4);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) bv[v4 + e] = t4[e];
+                    }
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * bv[v];
+                        for (int v = 0; v < kTW; ++v) acc[u][v] += av[u] * bv[v];
                 }
-                const bool fresh = c0 >= J0 && c0 < jb;  // panel columns become inverse columns: old value 0
+                // panel columns become inverse columns: old value 0. Columns of a tile right of its rows' diagonal
+                // (kTW > 4) receive values that are never read: X_b's substitution rewrites the block from I
+                const bool fresh = c0 >= J0 && c0 < jb;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     if (i0 + u >= n) continue;
-                    T* w = rr + u * pbo + c0;
-                    T o4[4] = {T(0), T(0), T(0), T(0)};
-                    if (!fresh) ld4(w, o4);
-                    st4(w, o4[0] - acc[u][0], o4[1] - acc[u][1], o4[2] - acc[u][2], o4[3] - acc[u][3]);
+#pragma unroll
+                    for (int v4 = 0; v4 < kTW; v4 += 4) {
+                        T* w = rr + u * pbo + c0 + v4;
+                        T o4[4] = {T(0), T(0), T(0), T(0)};
+                        if (!fresh) ld4(w, o4);
+                        st4(w, o4[0] - acc[u][v4], o4[1] - acc[u][v4 + 1], o4[2] - acc[u][v4 + 2],
+                            o4[3] - acc[u][v4 + 3]);
+                    }
                 }
             };
             if (ahead) {
                 const int G4 = (min(kNB, n - (b + 1) * kNB) + 3) / 4;
-                const int nd = G4 * (G4 + 1) / 2;  // diagonal tiles of block b+1
+                auto ndg = [&](int g) { return (4 * g + 4 + kTW - 1) / kTW; };  // diagonal-block tiles of group g
+                int nd = 0;
+                for (int g = 0; g < G4; ++g) nd += ndg(g);
                 for (int t = tid; t < nd; t += kCcThreads) {
                     int g = 0, rem = t;
-                    while (rem > g) { rem -= g + 1; ++g; }
-                    run(b + 1, g, jb + rem * 4);
+                    while (rem >= ndg(g)) { rem -= ndg(g); ++g; }
+                    run(b + 1, g, jb + rem * kTW);
                 }
                 __syncthreads();
                 if (warp == 0) factor_block(b + 1);
