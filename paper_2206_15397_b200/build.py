@@ -12,6 +12,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xptxas", "-warn-spills"]
+# A/B switches for the build macros (e.g. RKFAC_NVCC_DEFS="-DRKFAC_EA_CIN_RING=4"; rebuild with -f)
+FLAGS += os.environ.get("RKFAC_NVCC_DEFS", "").split()
 
 
 def sources() -> list[str]:

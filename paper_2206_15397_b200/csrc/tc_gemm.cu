@@ -47,7 +47,10 @@ constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
 //           output written in place) and two mirror chunks, all dense 128-byte rows in the TMA SWIZZLE_128B layout:
 //           each output chunk and its transpose leave by TMA bulk-tensor stores, so the epilogue -- a pure HBM
 //           stream -- keeps several chunks in flight per warp with a handful of instructions per chunk
-constexpr int kCinRing = 3;
+#ifndef RKFAC_EA_CIN_RING
+#define RKFAC_EA_CIN_RING 3  // Cin chunks per epilogue warp in the EA configuration (4 fills the 192 KB exactly)
+#endif
+constexpr int kCinRing = RKFAC_EA_CIN_RING;
 template <int kCfg>
 struct StageCfg {
     static constexpr int kSub = kCfg == 1 ? 2 : 1;
