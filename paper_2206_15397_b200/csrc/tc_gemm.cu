@@ -166,6 +166,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// split form: issue the TMEM load, overlap other waits, then wait with the registers as operands (so no use of them
+// can be scheduled above the wait)
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float load_mn(const float* p, long long ld, int t, int m, int n) {
@@ -609,7 +632,15 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kMaxBN;
             for (int c0 = 0; c0 < pr.n_tile; c0 += 32) {
                 uint32_t r[32];
-                tmem_ld32(tbase + c0, r);
+                if constexpr (kCfg == 2) {
+                    // the TMEM load in flight while this chunk's Cin cp.async group is awaited (every EA tile has a
+                    // Cin, host-checked: chunk_no's slot is complete once at most one younger group is pending)
+                    tmem_ld32_issue(tbase + c0, r);
+                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCinRing - 2) : "memory");
+                    tmem_ld32_wait(r);
+                } else {
+                    tmem_ld32(tbase + c0, r);
+                }
                 const int nbase = tl.n0 + c0;
                 if (pr.ksplit > 1) {  // raw partials, column-major per slice: each store is 128 B across the warp
                     if (m < pr.M) {
@@ -633,11 +664,8 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     for (int j = 0; j < 32; ++j) v[j] *= (nbase + j < nlim) ? pr.cs[nbase + j] : 0.f;
                 }
                 if constexpr (kCfg == 2) {
-                    // every EA tile has a Cin (host-checked): chunk_no's slot is complete once at most one younger
-                    // group (the next chunk's) is pending
-                    const int slot = chunk_no % kCinRing;
+                    const int slot = chunk_no % kCinRing;  // its cp.async group was awaited with the TMEM load
                     unsigned char* cs = ring + slot * kChunkBytes;
-                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCinRing - 2) : "memory");
                     __syncwarp();
 #pragma unroll
                     for (int j4 = 0; j4 < 32; j4 += 4) {
