@@ -51,16 +51,19 @@ constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
 #define RKFAC_EA_CIN_RING 3  // Cin chunks per epilogue warp in the EA configuration (4 fills the 192 KB exactly)
 #endif
 constexpr int kCinRing = RKFAC_EA_CIN_RING;
+#ifndef RKFAC_EA_STAGES
+#define RKFAC_EA_STAGES 3  // mainloop stages of the EA configuration (4 fits with RKFAC_EA_CIN_RING=2)
+#endif
 template <int kCfg>
 struct StageCfg {
     static constexpr int kSub = kCfg == 1 ? 2 : 1;
-    static constexpr int kStages = kCfg == 0 ? 4 : 3;
+    static constexpr int kStages = kCfg == 0 ? 4 : (kCfg == 2 ? RKFAC_EA_STAGES : 3);
     static constexpr int kBTile = kCfg == 2 ? kBM * kBK * 4 : kBTileBytes;
     static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTile;
 };
 constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 4 * 48 KB
 constexpr int kChunkBytes = 32 * 32 * 4;                                   // dense swizzled 32 x 32 chunk
-constexpr int kEaRingOff = 3 * StageCfg<2>::kStageBytes;                   // 96 KB
+constexpr int kEaRingOff = StageCfg<2>::kStages * StageCfg<2>::kStageBytes;  // 96 KB
 constexpr int kEaMirOff = kEaRingOff + 4 * kCinRing * kChunkBytes;         // 144 KB
 static_assert(kEaMirOff + 4 * 2 * kChunkBytes <= kStagesBytesMax, "EA smem");
 // byte offset of element (row r, column c) of a dense 32 x 32 FP32 chunk in the SWIZZLE_128B layout
