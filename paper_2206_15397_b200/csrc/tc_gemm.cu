@@ -52,7 +52,7 @@ constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
 #endif
 constexpr int kCinRing = RKFAC_EA_CIN_RING;
 #ifndef RKFAC_EA_STAGES
-#define RKFAC_EA_STAGES 3  // mainloop stages of the EA configuration (4 fits with RKFAC_EA_CIN_RING=2)
+#define RKFAC_EA_STAGES 4  // mainloop stages of the EA configuration (its region reaches 208 KB; 3: 6 % slower)
 #endif
 template <int kCfg>
 struct StageCfg {
@@ -65,7 +65,8 @@ constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 
 constexpr int kChunkBytes = 32 * 32 * 4;                                   // dense swizzled 32 x 32 chunk
 constexpr int kEaRingOff = StageCfg<2>::kStages * StageCfg<2>::kStageBytes;  // 96 KB
 constexpr int kEaMirOff = kEaRingOff + 4 * kCinRing * kChunkBytes;         // 144 KB
-static_assert(kEaMirOff + 4 * 2 * kChunkBytes <= kStagesBytesMax, "EA smem");
+constexpr int kEaRegionBytes = kEaMirOff + 4 * 2 * kChunkBytes;
+constexpr int kCfgRegionBytes(int cfg) { return cfg == 2 && kEaRegionBytes > kStagesBytesMax ? kEaRegionBytes : kStagesBytesMax; }
 // byte offset of element (row r, column c) of a dense 32 x 32 FP32 chunk in the SWIZZLE_128B layout
 __device__ __forceinline__ uint32_t sw128(int r, int c) {
     return (uint32_t)(r * 128 + ((((c >> 2) ^ (r & 7)) & 7) << 4) + (c & 3) * 4);
@@ -84,6 +85,8 @@ struct __align__(8) SmemBarriers {
 };
 constexpr int kBarrierBytes = (sizeof(SmemBarriers) + 127) / 128 * 128;
 constexpr int kStageTileBytes = 4 * 32 * 36 * 4;  // one 32x36 transpose tile per epilogue warp
+// the EA configuration stores its diagonal chunks by TMA too (no transpose tiles): its region may use their space
+static_assert(kEaRegionBytes <= kStagesBytesMax + kStageTileBytes, "EA smem");
 
 // ------------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -424,8 +427,8 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     // 1024-byte aligned base, derived by indexing the __shared__ array (integer round-trips of the address would
     // lose the address space: every smem access below would compile to generic LD/ST)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kStagesBytesMax);
-    float (*stage_tiles)[32][36] =
+    SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(smem + kCfgRegionBytes(kCfg));
+    float (*stage_tiles)[32][36] =  // unused by kCfg 2 when its region extends past kStagesBytesMax
         reinterpret_cast<float (*)[32][36]>(smem + kStagesBytesMax + kBarrierBytes);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int t_begin = cta_begin[blockIdx.x], t_end = cta_begin[blockIdx.x + 1];
@@ -694,9 +697,16 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         }
                     } else {
                         __syncwarp();
-                        if (nbase == mbase)  // the 32 x 32 diagonal chunk: upper part + mirror, per element
-                            chunk_store(v, pr.o[0], pr.ldo[0], 0, false, mbase, nbase, pr.M, nlim, true, true,
-                                        tile, lane);
+                        if (nbase == mbase) {
+                            // the 32 x 32 diagonal chunk: its strictly lower part replaced in place by the mirror of
+                            // the upper part (exact symmetry), then stored by TMA like any other chunk
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j > lane) *reinterpret_cast<float*>(cs + sw128(j, lane)) = v[j];
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) tma_store_2d(maps + kMapsPerProb * tl.prob + 4, cs, nbase, mbase);
+                        }
                         // chunks below the diagonal block are the mirrors of chunks above it: nothing to store
                     }
                     if (lane == 0) {
