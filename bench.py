@@ -33,7 +33,7 @@ OMEGA_ROOT = 7
 GRAD_ROOT = 99
 # dram__bytes_read.sum + dram__bytes_write.sum of one X*Q launch (ncu --set full, profiles/r01_xq_full.txt); None
 # until captured
-XQ_TRAFFIC = 626701824 + 21356288  # bytes, profiles/r01_xq_full.txt (X read once; its lo plane is formed in smem)
+XQ_TRAFFIC = 626528768 + 20797952  # bytes, profiles/r01_xq_full.txt (X read once; its lo plane is formed in smem)
 
 VGG_A = [28, 577, 577, 1153, 1153, 2305, 2305, 2305, 4609, 4609, 4609, 4609, 4609, 513, 513, 513]
 VGG_G = [64, 64, 128, 128, 256, 256, 256, 512, 512, 512, 512, 512, 512, 512, 512, 10]

@@ -42,13 +42,15 @@ constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
 // Three shared-memory configurations of the same ~192 KB region:
 //   kCfg 0, single tiles: 4 stages of [A hi][A lo][B hi][B lo] = 48 KB
 //   kCfg 1, paired tiles: 3 stages of [A0 hi][A1 hi][A0 lo][A1 lo][B hi][B lo] = 64 KB (256 rows share the B tile)
-//   kCfg 2, EA update (symmetric 128 x 128 tiles, axpy input Cin): 3 stages of 32 KB (B tile of 128 rows) and, in
-//           the space freed, per epilogue warp a ring of kCinRing 32 x 32 chunks (Cin prefetched by cp.async, the
-//           output written in place) and two mirror chunks, all dense 128-byte rows in the TMA SWIZZLE_128B layout:
-//           each output chunk and its transpose leave by TMA bulk-tensor stores, so the epilogue -- a pure HBM
-//           stream -- keeps several chunks in flight per warp with a handful of instructions per chunk
+//   kCfg 2, EA update (symmetric 128 x 128 tiles, axpy input Cin): RKFAC_EA_STAGES (4) stages of 32 KB (B tile of
+//           128 rows) and, after them, per epilogue warp a ring of kCinRing 32 x 32 chunks (Cin prefetched by
+//           cp.async, the output written in place) and two mirror chunks, all dense 128-byte rows in the TMA
+//           SWIZZLE_128B layout: each output chunk and its transpose leave by TMA bulk-tensor stores (the diagonal
+//           chunk after its lower part is overwritten by the mirror of its upper part), so the epilogue -- a pure
+//           HBM stream -- keeps several chunks in flight per warp with a handful of instructions per chunk; with no
+//           transpose tiles this region (208 KB) extends into their space and the barriers follow it
 #ifndef RKFAC_EA_CIN_RING
-#define RKFAC_EA_CIN_RING 3  // Cin chunks per epilogue warp in the EA configuration (4 fills the 192 KB exactly)
+#define RKFAC_EA_CIN_RING 3  // Cin chunks per epilogue warp in the EA configuration
 #endif
 constexpr int kCinRing = RKFAC_EA_CIN_RING;
 #ifndef RKFAC_EA_STAGES
