@@ -461,14 +461,22 @@ void Plan::build_ea_stage(double rho, double scale) {
     ea_simt_.reset();
     std::vector<SplitDesc> sm;
     long long off = 0;
+    ea_split_n_ = 0;
     if (ea_tc_) {
+        // the samples' lo planes: formed in smem by the converter warps for short K (VGG16, n = 128: 0.218 vs
+        // 0.256 ms with the split pass), stored by a split pass for long K, where the converters bound the mainloop
+        // (config 5, n = 512: 7.8 vs 12.1 ms); RKFAC_EA_STORED_LO=0/1 forces either
+        long long nmax = 0;
+        for (auto& F : f_) nmax = std::max<long long>(nmax, F.M ? F.n : 0);
+        bool stored_lo = nmax >= 512;
+        if (const char* e = std::getenv("RKFAC_EA_STORED_LO")) stored_lo = std::atoi(e) != 0;
         ea_tc_stage_ = new_tc();
         for (auto& F : f_) {
             if (!F.M || F.n == 0) continue;
             TcProblemDesc p;
             p.M = F.d; p.N = F.d; p.K = (int)F.n;
-            p.A = F.M; p.A_lo = nullptr; p.lda = F.ldm;  // both lo planes of the samples formed in smem
-            p.B = F.M; p.B_lo = nullptr; p.ldb = F.ldm;
+            p.A = F.M; p.A_lo = stored_lo ? F.Ml : nullptr; p.lda = F.ldm;  // default: both lo planes formed in smem
+            p.B = F.M; p.B_lo = stored_lo ? F.Ml : nullptr; p.ldb = F.ldm;
             p.sym = 1;
             p.alpha = (float)((1.0 - rho) * scale * scale);
             p.beta = (float)rho;
@@ -479,6 +487,7 @@ void Plan::build_ea_stage(double rho, double scale) {
             off += (long long)F.d * F.n;
         }
         ea_tc_stage_->finalize();
+        if (stored_lo) ea_split_n_ = (int)sm.size();
     } else {
         ea_simt_ = std::make_unique<GemmBatch>(GemmKind::F32);
         for (auto& F : f_) {
@@ -597,6 +606,7 @@ void Plan::ea_update(double rho, double scale) {
     cudaStream_t s = ctx_->stream;
     mark(kEA, true);
     if (ea_tc_) {
+        if (ea_split_n_ > 0) launch_split(d_split_m_.as<SplitDesc>(), ea_split_n_, split_m_total_, s);
         ea_tc_stage_->launch(s);
     } else {
         ea_simt_->launch(s);

@@ -132,6 +132,7 @@ class Plan {
     bool factors_bound_ = false, samples_bound_ = false;
     bool x_tma_ok_ = true;   // every bound X is a valid TMA operand (else a padded copy is made per decomposition)
     bool ea_tc_ = false;     // EA runs on the tensor-core path (needs TMA-valid X and samples)
+    int ea_split_n_ = 0;     // > 0: the samples' TF32 lo planes are stored by a split pass (RKFAC_EA_STORED_LO=1)
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
     // xqf_: the final X*Q (input of the core) with short accumulation chains (see kSliceK in engine.cu)
