@@ -122,6 +122,9 @@ int rkfac_plan_bind_samples(rkfac_plan_t plan, const float* const* samples_dev, 
 int rkfac_plan_bind_layers(rkfac_plan_t plan, int nlayers, const int* a_idx, const int* g_idx,
                            const float* const* grads_dev, float* const* outs_dev, float* const* mids_dev);
 
+/* How the EA update gets the samples' TF32 lo planes (3xTF32 operands): -1 automatic (default: stored by a split
+ * pass when some n >= 512, else formed in shared memory), 0 formed in shared memory, 1 stored.  Same arithmetic. */
+int rkfac_plan_set_ea_lo_mode(rkfac_plan_t plan, int mode);
 /* All factors: mbar <- rho*mbar + (1-rho)*scale^2 * m m^T (one launch). */
 int rkfac_plan_ea_update(rkfac_plan_t plan, double rho, double scale);
 /* All factors: rand-EVD with Omega_f from RngState(rng_root).substream(step, tag_f) (optimizer.hpp:189, 202),

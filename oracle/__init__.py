@@ -200,7 +200,8 @@ class Ref(Port):
                            C.c_size_t, C.c_size_t, C.c_int, _dp)
         self._step = L.fn("step_threaded", C.c_int, C.c_int, C.c_int, C.c_size_t, _szp, _szp,
                           C.POINTER(_dp), C.POINTER(_dp), _szp, C.c_double, C.c_size_t, C.c_size_t, C.c_size_t,
-                          C.c_uint64, C.c_uint64, C.c_double, C.POINTER(_dp), C.POINTER(_dp), _dp)
+                          C.c_uint64, C.c_uint64, C.c_double, C.POINTER(_dp), C.POINTER(_dp), _dp,
+                          C.POINTER(_dp), C.POINTER(_dp))
 
     def splitmix64(self, x):
         return self._port.splitmix64(x)
@@ -239,8 +240,9 @@ class Ref(Port):
         return self._port.synthetic_m(*a, **k)
 
     def step_threaded(self, method: str, threads: int, dims_a, dims_g, factors, ms, ns, rho, r, p, q,
-                      rng_root, step, lam, grads, outs):
-        """The reference's EA -> decompositions -> preconditioning over layers, one factor per thread."""
+                      rng_root, step, lam, grads, outs, us=None, dvs=None):
+        """The reference's EA -> decompositions -> preconditioning over layers, one factor per thread.  Optional
+        us / dvs (per factor, d x min(r, d) and min(r, d) FP64 arrays) receive the decompositions."""
         nl = len(dims_a)
         A = (C.c_size_t * nl)(*dims_a)
         G = (C.c_size_t * nl)(*dims_g)
@@ -249,9 +251,11 @@ class Ref(Port):
         nn = (C.c_size_t * (2 * nl))(*ns) if ns is not None else None
         gp = (_dp * nl)(*[_ptr(g) for g in grads]) if grads is not None else None
         op = (_dp * nl)(*[_ptr(o) for o in outs]) if outs is not None else None
+        up = (_dp * (2 * nl))(*[_ptr(u) for u in us]) if us is not None else None
+        dp = (_dp * (2 * nl))(*[_ptr(x) for x in dvs]) if dvs is not None else None
         ph = np.zeros(3)
         st = self._step(0 if method == "srevd" else 1, threads, nl, A, G, fp, mp, nn, rho, r, p, q, rng_root,
-                        step, lam, gp, op, _ptr(ph))
+                        step, lam, gp, op, _ptr(ph), up, dp)
         if st:
             raise OracleError(st, "step_threaded")
         return ph

@@ -121,12 +121,14 @@ int ref_apply_lowrank(const double* u, const double* dv, std::size_t dim, std::s
 // decompose A (which=0) and G (which=1) with substream(step, 2l+which), then LEFT_G(RIGHT_A(J))),
 // plus one EA update per factor beforehand.  Work is spread one factor (then one layer) per
 // std::thread over `threads` workers.  Pointers are per factor / per layer arrays.  Used as the
-// timed CPU baseline; times are reported back per phase in seconds.
+// timed CPU baseline; times are reported back per phase in seconds.  us/dvs (optional, per factor,
+// d x r_f row-major and r_f) receive the decompositions for parity checks.
 int ref_step_threaded(int method, int threads, std::size_t nlayers, const std::size_t* dims_a,
                       const std::size_t* dims_g, double* const* factors, const double* const* ms,
                       const std::size_t* ns, double rho, std::size_t r, std::size_t p, std::size_t q,
                       std::uint64_t rng_root, std::uint64_t step, double lambda,
-                      const double* const* grads, double* const* outs, double* phase_seconds) {
+                      const double* const* grads, double* const* outs, double* phase_seconds,
+                      double* const* us, double* const* dvs) {
     using Clock = std::chrono::steady_clock;
     const std::size_t nf = 2 * nlayers;
     std::vector<int> status(nf + nlayers, 0);
@@ -165,6 +167,8 @@ int ref_step_threaded(int method, int threads, std::size_t nlayers, const std::s
             const SketchParams sk{r, p, q};
             dec[f] = method == 0 ? srevd(to_mat(factors[f], d, d), sk, sub)
                                  : rsvd_psd(to_mat(factors[f], d, d), sk, sub);
+            if (us && us[f]) std::memcpy(us[f], dec[f].u.data(), sizeof(double) * dec[f].u.size());
+            if (dvs && dvs[f]) std::copy(dec[f].d.begin(), dec[f].d.end(), dvs[f]);
         });
     });
     auto t2 = Clock::now();

@@ -112,6 +112,7 @@ SIGNATURES = {
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "rkfac_plan_set_timing": (C.c_int, [_vp, C.c_int]),
+    "rkfac_plan_set_ea_lo_mode": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_set_max_ctas": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_prepare": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double]),
 }
@@ -504,6 +505,10 @@ class BatchedStep:
 
     def set_timing(self, on: bool):
         _check(self.ctx.lib.rkfac_plan_set_timing(self.h, 1 if on else 0), self.ctx.h, "set_timing")
+
+    def set_ea_lo_mode(self, mode: int):
+        """EA operands' TF32 lo planes: -1 automatic, 0 formed in shared memory, 1 stored by a split pass."""
+        _check(self.ctx.lib.rkfac_plan_set_ea_lo_mode(self.h, int(mode)), self.ctx.h, "set_ea_lo_mode")
 
     TIMING_KINDS = ("ea", "decompose", "precondition", "xq_gemm", "orth", "eig", "step")
 

@@ -319,6 +319,10 @@ int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas) {
     });
 }
 
+int rkfac_plan_set_ea_lo_mode(rkfac_plan_t plan, int mode) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_ea_lo_mode(mode); });
+}
+
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_timing(enabled != 0); });
 }

@@ -215,8 +215,14 @@ void Plan::bind_factors(float* const* X, const long long* ldx, float* const* Ut,
     ap_lambda_ = -1;
 }
 
+void Plan::set_ea_lo_mode(int mode) {
+    RKFAC_REQUIRE(mode >= -1 && mode <= 1, RKFAC_INVALID_ARGUMENT, "EA lo mode must be -1, 0 or 1");
+    ea_lo_mode_ = mode;
+    ea_rho_ = -1;  // rebuilt on the next EA update
+}
+
 void Plan::bind_samples(const float* const* M, const int64_t* n) {
-    bool ok = x_tma_ok_;
+    bool ok = true;
     Carver c;
     std::vector<size_t> off(f_.size());
     for (size_t i = 0; i < f_.size(); ++i) {
@@ -230,7 +236,7 @@ void Plan::bind_samples(const float* const* M, const int64_t* n) {
     }
     ml_arena_.alloc(c.off);
     for (size_t i = 0; i < f_.size(); ++i) f_[i].Ml = at<float>(ml_arena_, off[i]);
-    ea_tc_ = ok;
+    samples_tma_ok_ = ok;
     samples_bound_ = true;
     ea_rho_ = -1;
 }
@@ -462,6 +468,8 @@ void Plan::build_ea_stage(double rho, double scale) {
     std::vector<SplitDesc> sm;
     long long off = 0;
     ea_split_n_ = 0;
+    // decided from the operands bound NOW (factors and samples may be re-bound in either order)
+    ea_tc_ = x_tma_ok_ && samples_tma_ok_;
     if (ea_tc_) {
         // the samples' lo planes: formed in smem by the converter warps for short K (VGG16, n = 128: 0.218 vs
         // 0.256 ms with the split pass), stored by a split pass for long K, where the converters bound the mainloop
@@ -470,6 +478,7 @@ void Plan::build_ea_stage(double rho, double scale) {
         for (auto& F : f_) nmax = std::max<long long>(nmax, F.M ? F.n : 0);
         bool stored_lo = nmax >= 512;
         if (const char* e = std::getenv("RKFAC_EA_STORED_LO")) stored_lo = std::atoi(e) != 0;
+        if (ea_lo_mode_ >= 0) stored_lo = ea_lo_mode_ == 1;
         ea_tc_stage_ = new_tc();
         for (auto& F : f_) {
             if (!F.M || F.n == 0) continue;

@@ -94,6 +94,9 @@ class Plan {
                      float* const* mid);
     void set_tags(const uint64_t* tags);
     void set_explicit_seed(int f, uint64_t seed, uint64_t ctr0);
+    // EA operands' TF32 lo planes: -1 automatic (stored by a split pass when n >= 512), 0 formed in shared memory,
+    // 1 stored by a split pass (arithmetic identical; rkfac_plan_set_ea_lo_mode)
+    void set_ea_lo_mode(int mode);
 
     void ea_update(double rho, double scale);
     // mode 1: seeds from substream(root, step, tag); mode 0: explicit seeds.
@@ -131,7 +134,9 @@ class Plan {
     DevBuf arena_, layer_arena_, ml_arena_;
     bool factors_bound_ = false, samples_bound_ = false;
     bool x_tma_ok_ = true;   // every bound X is a valid TMA operand (else a padded copy is made per decomposition)
-    bool ea_tc_ = false;     // EA runs on the tensor-core path (needs TMA-valid X and samples)
+    bool samples_tma_ok_ = false;  // every bound sample matrix is a valid TMA operand
+    bool ea_tc_ = false;     // EA runs on the tensor-core path (needs TMA-valid X and samples; set by build_ea_stage)
+    int ea_lo_mode_ = -1;    // see set_ea_lo_mode
     int ea_split_n_ = 0;     // > 0: the samples' TF32 lo planes are stored by a split pass (RKFAC_EA_STORED_LO=1)
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).

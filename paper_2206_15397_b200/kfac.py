@@ -41,7 +41,7 @@ class ScheduleOverrides:  # optimizer.hpp:30-36
 
 @dataclass
 class OptimizerConfig:  # optimizer.hpp:38-53
-    method: Method = Method.SRE_KFAC
+    method: Method = Method.KFAC  # the reference default (optimizer.hpp:39)
     rho: float = 0.95
     t_ku: int = 10        # factor-update period
     n_pwr_it: int = 4     # sketch power iterations

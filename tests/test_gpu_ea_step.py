@@ -1,0 +1,209 @@
+"""GPU parity of the paths the bench times, at the sizes it times them (VERDICT r01 "next" #1):
+
+* the plan's tcgen05 EA update (kfactor.hpp:33-41) on multi-tile factors -- off-diagonal mirrored TMA stores,
+  multi-tile Cin reads of the in-place factor -- with the samples' TF32 lo planes formed in shared memory (VGG16,
+  n = 128) and stored by the split pass (config 5, n >= 512), from zero and identity init;
+* the whole BASELINE config-3 step exactly as bench.py runs it (20 zero-init EA warm-ups through the plan,
+  StreamedStep(groups=5), step(7, 0, 0.1)) against the reference's own step (oracle/_ref ref_step_threaded:
+  optimizer.hpp:139-167 over the unmodified reference headers) on the same FP64 inputs.
+
+Tolerances: EA rel. Frobenius error <= 3e-8 * n per factor, exact symmetry.  The bound is linear in K = n because
+the tensor core's FP32 accumulation truncates (tools/tc_acc.cu): every kind::tf32 MMA (K = 8, three per step in
+3xTF32) adds with round-toward-zero, a biased loss of up to one accumulator ulp.  Measured on B200 (zero init, one
+product dominates): 2.6e-6 at n = 128, 5.2e-6 at n = 256, 9.4e-6 at n = 512 (~2e-8 * n); from identity init 4e-8.
+Step: north_star's 1e-4 on the reconstruction U L U^T, the top-r eigenvalues and the preconditioned gradients.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import GRAD_ROOT, OMEGA_ROOT, ROOT_SEED, eig_err, recon_err, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+EA_TOL_PER_K = 3e-8
+TOL = 1e-4
+
+
+def np64(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _ea_case(port, cuda, layers, n, e, mode, steps_zero, steps_eye):
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    st = rk.BatchedStep(layers, rank=16, oversampling=4, power_iters=1, method=rk.DecompMethod.SREVD,
+                        n_samples=[n], device=0)
+    if mode is not None:
+        st.set_ea_lo_mode(mode)
+    dims = st.dims
+    results = []
+    for init, steps in (("zero", steps_zero), ("eye", steps_eye)):
+        xs = [np.zeros((d, d)) if init == "zero" else np.eye(d) for d in dims]
+        for f, d in enumerate(dims):
+            st.factors[f].copy_(torch.as_tensor(xs[f], dtype=torch.float32, device=cuda))
+        for k in range(steps):
+            ms = []
+            for f, d in enumerate(dims):
+                m = port.synthetic_m(ROOT_SEED, k, f, n, d, e).astype(np.float32)
+                st.samples[f].copy_(torch.as_tensor(m, device=cuda))
+                ms.append(m.astype(np.float64))
+            st.ea_update(0.95, 1.0)
+            xs = oracle.parallel_map(lambda f: port.ea_update(xs[f], ms[f], 0.95), range(len(dims)),
+                                     min(8, os.cpu_count() or 1))
+        torch.cuda.synchronize()
+        got = [np64(x) for x in st.factors]
+        for f, d in enumerate(dims):
+            err = rel_fro(got[f], xs[f])
+            print(f"EA {init} f={f} d={d} n={n} mode={mode}: rel err {err:.2e}")
+            assert err < EA_TOL_PER_K * n, (init, f, d, err)
+            assert np.array_equal(got[f], got[f].T), (init, f, d)  # kfactor.hpp:39 symmetrize: exact
+        results.append([x.clone() for x in st.factors])
+    return results
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_plan_ea_multitile_n128_matches_oracle(port, cuda, mode):
+    """VGG16-sized factors (n = 128): 577 (5 row tiles), 1153 (10), 4609 (37, off-diagonal mirrors) and a 64-wide one,
+    in one grouped launch, lo planes formed in smem (mode 0, the bench's default at n = 128) and stored (mode 1)."""
+    import paper_2206_15397_b200 as rk
+
+    _ea_case(port, cuda, [rk.LayerSpec(577, 1153), rk.LayerSpec(4609, 64)], 128, 1.0, mode, 3, 2)
+
+
+def test_plan_ea_lo_modes_are_bitwise_equal(port, cuda):
+    """Forming the samples' TF32 lo planes in shared memory or storing them gives the same arithmetic."""
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    layers = [rk.LayerSpec(1153, 300)]
+    a = _ea_case(port, cuda, layers, 256, 1.0, 0, 2, 0)
+    b = _ea_case(port, cuda, layers, 256, 1.0, 1, 2, 0)
+    for x, y in zip(a[0], b[0]):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("mode", [None, 0])
+def test_plan_ea_long_k_n512_matches_oracle(port, cuda, mode):
+    """Config-5-style long K (n = 512): the automatic mode stores the samples' lo planes by the split pass (the path
+    config 5 runs); mode 0 forms them in smem."""
+    import paper_2206_15397_b200 as rk
+
+    _ea_case(port, cuda, [rk.LayerSpec(2048, 640)], 512, 1.2, mode, 3, 1)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref (the reference build) not present")
+def test_config3_full_step_as_benched_matches_reference(cuda):
+    """BASELINE config 3, the bench's workload, through the bench's own code path; the reference's whole step
+    (EA -> 32 srevd -> 16 RIGHT/LEFT preconditionings, ref_step_threaded over the unmodified reference headers) on
+    the same inputs: the GPU's FP32 factors after the 20 warm-up EA steps, the timed step's samples and gradients."""
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    import bench
+
+    layers, n, e, r, p, q, lam, warm = bench.WORKLOADS["vgg16"]
+    specs = [rk.LayerSpec(a, g) for a, g in layers]
+    st = rk.StreamedStep(specs, groups=5, rank=r, oversampling=p, power_iters=q, method=rk.DecompMethod.SREVD,
+                         n_samples=[n], device=0)
+    inv_sqrt_n = 1.0 / math.sqrt(n)
+
+    def fill_samples(k):  # bench.run_ours.fill_samples
+        for f, d in enumerate(st.dims):
+            z = rk.sample_gaussian(rk.RngState(rk.substream_seed(ROOT_SEED, k, f)), n, d, device=cuda)
+            s = torch.arange(1, d + 1, device=cuda, dtype=torch.float64).pow(-e)
+            st.samples[f].copy_((z.double() * s[None, :] * inv_sqrt_n).t().float())
+
+    for k in range(warm):
+        fill_samples(k)
+        st.ea_update(0.95, 1.0)
+    fill_samples(warm)
+    for l, (a, g) in enumerate(layers):
+        st.grads[l].copy_(rk.sample_gaussian(rk.RngState(rk.substream_seed(GRAD_ROOT, l, 0)), g, a, device=cuda))
+    torch.cuda.synchronize()
+    factors = [np.ascontiguousarray(np64(x)) for x in st.factors]  # the step's inputs, FP32 values as FP64
+    ms = [np.ascontiguousarray(np64(x)) for x in st.samples]
+    grads = [np.ascontiguousarray(np64(x)) for x in st.grads]
+    st.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
+    torch.cuda.synchronize()
+
+    outs = [np.zeros((g, a)) for a, g in layers]
+    ref = oracle.ref()
+    dims_a = [a for a, _ in layers]
+    dims_g = [g for _, g in layers]
+    threads = os.cpu_count() or 1
+    us = [np.zeros((d, min(r, d))) for d in st.dims]
+    dvs = [np.zeros(min(r, d)) for d in st.dims]
+    ph = ref.step_threaded("srevd", threads, dims_a, dims_g, factors, ms, [n] * len(ms), 0.95, r, p, q, OMEGA_ROOT,
+                           0, lam, grads, outs, us, dvs)
+    print(f"reference step on {threads} threads: EA {ph[0]:.1f}s, srevd {ph[1]:.1f}s, apply {ph[2]:.1f}s")
+    decs = [(us[f], dvs[f], None) for f in range(len(us))]  # `factors` now hold the reference's EA result
+    worst = {"recon": 0.0, "eig": 0.0, "grad": 0.0, "ea": 0.0}
+    for f in range(len(factors)):
+        worst["ea"] = max(worst["ea"], rel_fro(np64(st.factors[f]), factors[f]))
+        lr = st.lowrank(f)
+        u0, d0, _ = decs[f]
+        worst["recon"] = max(worst["recon"], recon_err(np64(lr.u), np64(lr.d), u0, d0))
+        worst["eig"] = max(worst["eig"], eig_err(np64(lr.d), d0))
+    for l in range(len(layers)):
+        worst["grad"] = max(worst["grad"], rel_fro(np64(st.outs[l]), outs[l]))
+    print("config-3 step vs reference, worst over factors/layers:", worst)
+    assert worst["ea"] < EA_TOL_PER_K * n
+    assert worst["recon"] < TOL and worst["eig"] < TOL and worst["grad"] < TOL, worst
+
+
+GOLD5 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config5_golden.npz")
+
+
+@pytest.mark.skipif(not os.path.exists(GOLD5), reason="config-5 golden fixture not generated")
+def test_config5_pair_matches_reference_golden(port, cuda):
+    """BASELINE config 5 (d = 16384, n = 512, 10 EA steps, e = 1.2, r = 256, p = 16, q = 4, lambda = 0.05) against
+    the fixture tests/golden/make_config5_golden.py computed with the reference itself (oracle/_ref): the pair's top-r
+    eigenvalues and fixed random projections of X, U diag(d) U^T and the preconditioned gradient S.  The GPU builds
+    its factors exactly as bench.py does (samples from the device RNG, zero-init EA through the plan)."""
+    import torch
+    import paper_2206_15397_b200 as rk
+
+    g = np.load(GOLD5)
+    D, N, STEPS, R, P, Q = (int(v) for v in g["dims"])
+    E, RHO, LAM = (float(v) for v in g["params"])
+    st = rk.BatchedStep([rk.LayerSpec(D, D)], rank=R, oversampling=P, power_iters=Q, method=rk.DecompMethod.SREVD,
+                        n_samples=[N], device=0)
+    inv_sqrt_n = 1.0 / math.sqrt(N)
+    s = torch.arange(1, D + 1, device=cuda, dtype=torch.float64).pow(-E)
+
+    def fill(k):
+        for f in range(2):
+            z = rk.sample_gaussian(rk.RngState(rk.substream_seed(ROOT_SEED, k, f)), N, D, device=cuda)
+            st.samples[f].copy_((z.double() * s[None, :] * inv_sqrt_n).t().float())
+
+    for k in range(STEPS - 1):
+        fill(k)
+        st.ea_update(RHO, 1.0)
+    fill(STEPS - 1)  # the last EA update runs inside the step, as in bench.py
+    st.grads[0].copy_(rk.sample_gaussian(rk.RngState(rk.substream_seed(GRAD_ROOT, 0, 0)), D, D, device=cuda))
+    st.step(OMEGA_ROOT, 0, LAM, RHO, 1.0)
+    torch.cuda.synchronize()
+    sys_v, _ = port.sample_gaussian(5150001, 0, D, 3)  # make_config5_golden.sketch_vectors
+    sys_w, _ = port.sample_gaussian(5150002, 0, D, 3)
+    v = torch.as_tensor(sys_v, device=cuda)
+    w = torch.as_tensor(sys_w, device=cuda)
+    errs = {}
+    for f, tag in ((0, "a"), (1, "g")):
+        x = st.factors[f].double()
+        errs[f"xv_{tag}"] = rel_fro((x @ v).cpu().numpy(), g[f"xv_{tag}"])
+        lr = st.lowrank(f)
+        u, dv = lr.u.double(), lr.d.double()
+        errs[f"pv_{tag}"] = rel_fro((u @ (dv[:, None] * (u.T @ v))).cpu().numpy(), g[f"pv_{tag}"])
+        errs[f"eig_{tag}"] = eig_err(dv.cpu().numpy(), g[f"dvals_{tag}"])
+        del x
+    out = st.outs[0].double()
+    errs["sv"] = rel_fro((out @ v).cpu().numpy(), g["sv"])
+    errs["ws"] = rel_fro((w.T @ out).cpu().numpy(), g["ws"])
+    print("config 5 vs reference golden:", {k: f"{e:.2e}" for k, e in errs.items()})
+    assert errs["xv_a"] < EA_TOL_PER_K * N and errs["xv_g"] < EA_TOL_PER_K * N
+    assert max(errs[k] for k in ("pv_a", "pv_g", "eig_a", "eig_g", "sv", "ws")) < TOL, errs
