@@ -8,9 +8,10 @@ preconditioning of every layer gradient) on the BASELINE config-3 workload: the 
 Our arm: one process per GPU (torchrun for N>1), layers LPT-sharded across ranks, one NCCL all-gather of the
 preconditioned gradients.  A step = one EA update of every factor + rand-EVD of every factor + preconditioning of
 every layer (+ the all-gather).  value = factors inverted per second of whole step (all ranks) = 32 / step time.
-Reference arm (--impl reference): the reference's own C++ CPU code (oracle/_ref, the unmodified headers) on the
-box's host cores, one factor per std::thread, on a bounded sample of the same workload, extrapolated to the
-whole step (see `cpu_baseline.sample`).
+Reference arm (--impl reference): the reference's own C++ CPU code (oracle/_ref, the unmodified headers compiled
+with the reference's own flags) on all of the box's host cores, one factor per std::thread: every timed step is the
+WHOLE step of the workload, measured (config 5 alone -- hours per FP64 step -- is a proxy, extrapolated and labelled
+in `cpu_baseline.sample`).
 """
 from __future__ import annotations
 
@@ -31,9 +32,10 @@ UNIT = "inversions/s"
 ROOT_SEED = 220615397  # synthetic factor statistics
 OMEGA_ROOT = 7
 GRAD_ROOT = 99
-# dram__bytes_read.sum + dram__bytes_write.sum of one X*Q launch (ncu --set full, profiles/r01_xq_full.txt); None
-# until captured
-XQ_TRAFFIC = 626528768 + 20797952  # bytes, profiles/r01_xq_full.txt (X read once; its lo plane is formed in smem)
+# dram__bytes_read.sum + dram__bytes_write.sum of one X*Q launch of THIS workload, from that workload's own ncu --set
+# full capture (profiles/); None for a workload not captured yet
+XQ_TRAFFIC = {"vgg16": 626528768 + 20797952}  # X read once; its lo plane is formed in smem
+XQ_TRAFFIC_SRC = {"vgg16": "profiles/r01_xq_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"}
 
 VGG_A = [28, 577, 577, 1153, 1153, 2305, 2305, 2305, 4609, 4609, 4609, 4609, 4609, 513, 513, 513]
 VGG_G = [64, 64, 128, 128, 256, 256, 256, 512, 512, 512, 512, 512, 512, 512, 512, 10]
@@ -133,8 +135,67 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------------------- CPU baseline
+def _cpu_lib():
+    """The reference's own code compiled with its own flags (oracle/_ref/librkfac_ref_stock.so, CMakeLists.txt:9);
+    the parity build, then the restatement, only when that is absent (the kind says which)."""
+    import oracle
+
+    if oracle.ref_stock_available():
+        return oracle.ref_stock(), "reference", "oracle/_ref/librkfac_ref_stock.so (-O3 -march=native -funroll-loops)"
+    if oracle.ref_available():
+        return oracle.ref(), "reference", "oracle/_ref/librkfac_ref.so (-O3 -march=x86-64-v3 -ffp-contract=off)"
+    return oracle.port(), "port", "oracle/liboracle.so (C restatement)"
+
+
+class CpuStep:
+    """The reference's whole step on the same workload, MEASURED (no extrapolation): one EA update of every factor,
+    srevd of every factor (Omega from RngState(7).substream(0, f)), RIGHT_A then LEFT_G of every layer
+    (optimizer.hpp:139-167), one factor (then one layer) per std::thread over `threads` host cores (ref_step_threaded;
+    the functions are pure).  Inputs are built once, untimed: the factors after the workload's
+    EA warm-up (FP64, zero init, the synthetic statistics of SURVEY.md 8(d)), the timed step's samples and the
+    gradients, all from the reference RNG."""
+
+    def __init__(self, layers, n, e, r, p, q, lam, warm, threads=None):
+        import numpy as np
+
+        import oracle
+
+        self.lib, self.kind, self.build = _cpu_lib()
+        port = oracle.port()
+        self.layers, self.n, self.r, self.p, self.q, self.lam = layers, n, r, p, q, lam
+        self.threads = threads or os.cpu_count() or 1
+        dims = [d for a, g in layers for d in (a, g)]
+
+        def warm_factor(f):  # zero-init EA over `warm` steps in FP64 (numpy: kfactor.hpp:33-41 restated)
+            d = dims[f]
+            x = np.zeros((d, d))
+            for k in range(warm):
+                m = port.synthetic_m(ROOT_SEED, k, f, n, d, e)
+                x *= 0.95
+                x += 0.05 * (m @ m.T)
+                x = 0.5 * (x + x.T)
+            return x
+
+        self.factors0 = oracle.parallel_map(warm_factor, range(len(dims)), min(4, self.threads))
+        self.ms = [port.synthetic_m(ROOT_SEED, warm, f, n, d, e) for f, d in enumerate(dims)]
+        self.grads = [port.sample_gaussian(port.substream(GRAD_ROOT, l, 0), 0, g, a)[0] for l, (a, g) in
+                      enumerate(layers)]
+        self.outs = [np.zeros((g, a)) for a, g in layers]
+
+    def run(self, threads=None):
+        """One timed step (s) on `threads` cores; returns (seconds, per-phase seconds)."""
+        facs = [x.copy() for x in self.factors0]  # the EA updates in place: every step starts from the same state
+        nth = threads or self.threads
+        t0 = time.perf_counter()
+        ph = self.lib.step_threaded("srevd", nth, [a for a, _ in self.layers], [g for _, g in self.layers], facs,
+                                    self.ms, [self.n] * len(self.ms), 0.95, self.r, self.p, self.q, OMEGA_ROOT, 0,
+                                    self.lam, self.grads, self.outs)
+        return time.perf_counter() - t0, [float(x) for x in ph]
+
+
 def cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s, threads=None):
-    """The reference's own code (oracle/_ref) on a bounded sample of the workload, on `threads` host cores.
+    """Config 5 only (d = 16384: the reference's FP64 step takes hours): the reference's own code on a proxy of the
+    workload, on `threads` host cores, extrapolated (`cpu_baseline.sample` says so).
 
     The sample is the smallest layers (by decomposition cost) whose estimated makespan fits `budget_s`; the full
     step time is extrapolated as kappa * LPT-makespan(full) with kappa = measured / modelled sample time, the
@@ -143,7 +204,7 @@ def cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s, threads=None):
 
     import oracle
 
-    ref = oracle.best()
+    ref = _cpu_lib()[0]
     port = oracle.port()
     cores = threads or os.cpu_count() or 1
     fac, lay = work_model(layers, n, r, p, q)
@@ -251,29 +312,90 @@ def cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s, threads=None):
             "phase_seconds": None if ph is None else [float(x) for x in ph]}
 
 
+SINGLE_THREAD_FILE = os.path.join(ROOT, "profiles", "r02_cpu_1thread.json")
+
+
+def single_thread_record(workload):
+    """The reference's single-thread step on this workload, measured once on the GPU box's host by
+    `python bench.py --impl reference --cpu-threads 1 --steps 1` (a ~4-minute run, too long for every bench run) and
+    committed; reported next to the all-core figure with its provenance."""
+    try:
+        with open(SINGLE_THREAD_FILE) as fh:
+            rec = json.load(fh)
+        return rec if rec.get("config", {}).get("workload") == workload else None
+    except Exception:
+        return None
+
+
 def run_reference_arm(args, wl):
-    layers, n, e, r, p, q, lam, _ = wl
+    """The reference's own CPU implementation of the path (--impl reference): every timed step is the WHOLE step of
+    the workload (CpuStep: EA -> 32 srevd -> 16 preconditionings), measured, on all host cores.  One untimed warm-up
+    step (the CPU has nothing to JIT; it pages in the inputs); timed steps stop once 200 s of CPU time have been spent
+    so the run ends within a few minutes (`steps` is the count actually timed).  Config 5 (hours per FP64 step) is
+    the one workload measured on a proxy and extrapolated (cpu_reference_sample)."""
+    layers, n, e, r, p, q, lam, warm = wl
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    res = None
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference_sample(layers, n, e, r, p, q, lam, budget)
-        if i >= args.warmup:
-            vals.append(res["extrapolated_step_s"])
-    t = statistics.median(vals) if vals else res["extrapolated_step_s"]
     nf = 2 * len(layers)
+    threads = args.cpu_threads or os.cpu_count() or 1
+    if args.workload == "wide16384":
+        budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+        vals = []
+        for i in range(1 + args.steps):
+            res = cpu_reference_sample(layers, n, e, r, p, q, lam, budget, threads=threads)
+            if i >= 1:
+                vals.append(res["extrapolated_step_s"])
+        t, timed = statistics.median(vals), len(vals)
+        cpu = {k: res[k] for k in ("kind", "cores", "sample")}
+    else:
+        cs = CpuStep(layers, n, e, r, p, q, lam, warm, threads)
+        if args.warmup > 0:
+            cs.run()  # warm-up (skipped with --warmup 0, e.g. for the 4-minute single-thread record)
+        vals, phases, spent = [], [], 0.0
+        for i in range(args.steps):
+            s, ph = cs.run()
+            vals.append(s)
+            phases.append(ph)
+            spent += s
+            if spent + s > 200.0:
+                break
+        t, timed = statistics.median(vals), len(vals)
+        cpu = {"kind": cs.kind, "cores": threads,
+               "sample": f"the whole {args.workload} step ({nf} factors: EA update + srevd + RIGHT/LEFT apply), measured "
+                         f"{timed}x on {threads} host threads (one factor per std::thread); build {cs.build}; "
+                         f"median phase seconds EA/srevd/apply "
+                         f"{[round(statistics.median(x), 3) for x in zip(*phases)]}"}
     v = nf / t
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": timed, "steps_requested": args.steps, "warmup": min(1, args.warmup), "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "factors": nf, "layers": len(layers), "rank": r,
                        "oversampling": p, "power_iters": q, "lambda": lam, "n": n},
-            "cpu_baseline": {k: res[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+            "cpu_baseline": cpu | {"value": v, "unit": UNIT},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_line(args, wl):
+    """`cpu_baseline` of our arm (rank 0, N = 1): ONE measured whole step of the reference on all host cores (about 20 s
+    for VGG16 on 16 cores), plus the committed single-thread measurement; config 5 uses the extrapolated proxy."""
+    layers, n, e, r, p, q, lam, warm = wl
+    nf = 2 * len(layers)
+    threads = args.cpu_threads or os.cpu_count() or 1
+    if args.workload == "wide16384":
+        return cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s=args.cpu_budget, threads=threads)
+    cs = CpuStep(layers, n, e, r, p, q, lam, warm, threads)
+    t, ph = cs.run()
+    out = {"value": nf / t, "unit": UNIT, "cores": threads, "kind": cs.kind,
+           "sample": f"one whole {args.workload} step ({nf} factors: EA update + srevd + RIGHT/LEFT apply), measured "
+                     f"on {threads} host threads, one factor per std::thread; build {cs.build}",
+           "step_seconds": t, "phase_seconds": ph}
+    st = single_thread_record(args.workload)
+    if st:
+        out["single_thread"] = {"value": st["value"], "unit": UNIT, "step_seconds": st["ms_per_step"] / 1e3,
+                                "source": os.path.relpath(SINGLE_THREAD_FILE, ROOT)}
+    return out
 
 
 # -------------------------------------------------------------------------------------------- our arm
@@ -294,8 +416,11 @@ def run_ours(args, wl):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     costs = [layer_cost(a, g, r, p) for a, g in layers]
-    parts = lpt_partition(costs, world)
-    mine = parts[rank]
+    # --emulate-world N --emulate-rank k: run rank k's shard of an N-GPU job alone on this GPU (no collective), to
+    # measure every shard's critical path on a one-GPU box (tools/shard_projection.py)
+    part_world, part_rank = (args.emulate_world, args.emulate_rank) if args.emulate_world else (world, rank)
+    parts = lpt_partition(costs, part_world)
+    mine = parts[part_rank]
     sizes = [a * g for a, g in layers]
     layout = GatherLayout.build(sizes, parts)
     shapes = [(g, a) for a, g in layers]
@@ -464,8 +589,13 @@ def run_ours(args, wl):
     f_xq_launch = sum(f["f_xq_launch"] for f in mine_f)
     achieved = f_xq_launch / (xq_avg * 1e-3) / 1e12
     # 3xTF32 issues three tf32 MMAs per algorithmic FMA: its ceiling is the measured dense bf16 rate / 2 (TF32)
-    # / 3.  The kernel is timed inside a long step, so the sustained bf16 figure is the denominator.
-    tf32_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 2.0
+    # / 3.  The burst bf16 figure applies when the clock record of the timed region shows no power cap and the SM
+    # clock at its maximum (the kernel then runs at the clock the burst figure was measured at); else the sustained.
+    clocks = clk.summary()
+    capped = ("sw_power_cap" in clocks["reasons"] or clocks["sm_mhz"] is None or clocks["sm_max_mhz"] is None
+              or clocks["sm_mhz"] < 0.97 * clocks["sm_max_mhz"])
+    peak_key = "bf16_tflops_sustained" if capped else "bf16_tflops"
+    tf32_peak = peaks.get(peak_key, peaks["bf16_tflops"]) / 2.0
     xq_peak = tf32_peak / 3.0
     ea_ms = timing["ea"][0] / max(1, timing["ea"][1])
     ap_ms = timing["precondition"][0] / max(1, timing["precondition"][1])
@@ -476,9 +606,9 @@ def run_ours(args, wl):
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.emulate_world:
             try:
-                cpu = cpu_reference_sample(layers, n, e, r, p, q, lam, budget_s=args.cpu_budget)
+                cpu = cpu_baseline_line(args, wl)
             except Exception as ex:  # noqa: BLE001
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
         value = nf_total / (ms * 1e-3)
@@ -497,10 +627,13 @@ def run_ours(args, wl):
             "precond_step_ms": ms,
             "stage_ms": stages,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": xq_peak, "unit": "TFLOP/s",
-                         "frac": achieved / xq_peak, "traffic": XQ_TRAFFIC,
+                         "frac": achieved / xq_peak, "traffic": XQ_TRAFFIC.get(args.workload),
                          "kernel": "tc_gemm_kernel: grouped X*Q product (all factors, one launch), tcgen05 3xTF32",
-                         "peak_basis": f"{basis} sustained bf16 {peaks.get('bf16_tflops_sustained')} TF/s / 2 (TF32) "
-                                       f"/ 3 (3xTF32 MMAs per FMA)",
+                         "peak_basis": f"{basis} {'sustained' if capped else 'burst'} bf16 "
+                                       f"{peaks.get(peak_key, peaks['bf16_tflops'])} TF/s / 2 (TF32) / 3 (3xTF32 MMAs "
+                                       f"per FMA); {'power cap or clock below max' if capped else 'no cap, max clock'}"
+                                       f" in the timed region",
+                         "traffic_source": XQ_TRAFFIC_SRC.get(args.workload),
                          "frac_of_tf32": achieved / tf32_peak},
             "ea_hbm": {"achieved_gbs": ea_bytes / (ea_ms * 1e-3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
                        "frac": ea_bytes / (ea_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
@@ -510,8 +643,10 @@ def run_ours(args, wl):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches // max(1, args.steps),
             "gpu_launches_total": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
+            "emulated_shard": ({"world": part_world, "rank": part_rank, "layers": list(mine)} if args.emulate_world
+                               else None),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -526,10 +661,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="config 5 proxy sample budget (s)")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU baseline (0: all)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=5, help="layer groups on concurrent streams (StreamedStep; 5 gave the best e2e)")
     ap.add_argument("--profile-step", action="store_true", help="run one step under cudaProfilerStart/Stop and exit")
+    ap.add_argument("--emulate-world", type=int, default=0, help="run one shard of an N-GPU job alone (projection)")
+    ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
                     help="replay the timed step as one CUDA graph (rk.StepGraph); measured within 0.5 %% of eager")
     args = ap.parse_args()

@@ -133,8 +133,31 @@ int rkfac_plan_decompose(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
 int rkfac_plan_set_tags(rkfac_plan_t plan, const uint64_t* tags);
 /* All layers: outs = LEFT_G(RIGHT_A(grads)) (optimizer.hpp:159-162). */
 int rkfac_plan_precondition(rkfac_plan_t plan, double lambda);
-/* EA (if samples bound) -> decompose -> precondition (if layers bound). */
+/* EA (if samples bound) -> decompose -> precondition (if layers bound) -> all-gather (if rkfac_plan_set_gather). */
 int rkfac_plan_step(rkfac_plan_t plan, double rho, double scale, uint64_t rng_root, uint64_t step, double lambda);
+/* Device bytes the plan owns (the reference has no workspace: every op returns new matrices, matrix.hpp:14-65). */
+size_t rkfac_plan_workspace_size(rkfac_plan_t plan);
+
+/* ---- multi-GPU (BASELINE config 4): layers sharded over ranks, one NCCL all-gather ----------- */
+/* The reference is single-process (optimizer.hpp:145-165 loops over independent layers; SPEC.md:391 allows them to
+ * run concurrently): a rank decomposes and preconditions its own layers, then the packed preconditioned gradients
+ * are all-gathered over NVLink/NVSwitch.  NCCL (libnccl.so.2) is loaded on first use; its errors are
+ * RKFAC_NCCL_ERROR. */
+/* Writes a new clique's 128-byte ncclUniqueId to id_out (rank 0; ship it to the other ranks out of band). */
+int rkfac_nccl_unique_id(void* id_out);
+/* Joins the clique as `rank` of `nranks` (ncclCommInitRank: blocks until every rank joined) and attaches the
+ * communicator to the context, which owns it from then on. */
+int rkfac_nccl_init(rkfac_context_t ctx, const void* unique_id, int nranks, int rank);
+/* Attaches a caller-owned ncclComm_t instead. */
+int rkfac_set_nccl_comm(rkfac_context_t ctx, void* nccl_comm, int nranks, int rank);
+/* recv_dev (nranks * count floats, rank-major) <- every rank's send_dev (count floats), on the context stream. */
+int rkfac_allgather(rkfac_context_t ctx, const float* send_dev, float* recv_dev, int64_t count);
+/* rkfac_plan_step ends with the all-gather: layer l's output (d_G x d_A) is packed at offsets[l] (floats) of this
+ * rank's chunk of chunk_elems floats, and the chunks of all ranks land in gathered_dev (nranks * chunk_elems).
+ * gathered_dev = NULL turns it off. */
+int rkfac_plan_set_gather(rkfac_plan_t plan, int64_t chunk_elems, const int64_t* offsets, float* gathered_dev);
+/* The pack + all-gather alone (after rkfac_plan_precondition). */
+int rkfac_plan_gather(rkfac_plan_t plan);
 
 /* Stage timing with CUDA events on the context stream, recorded inside the calls and harvested after the caller
  * synchronises (no host sync inside a step).  set_timing(1) enables and resets.  rkfac_plan_timing fills 7 sums (ms)

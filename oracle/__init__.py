@@ -25,7 +25,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle.so")
-REF_SO = os.path.join(HERE, "_ref", "librkfac_ref.so")
+REF_SO = os.path.join(HERE, "_ref", "librkfac_ref.so")  # parity build (-ffp-contract=off, bit-pinned)
+REF_STOCK_SO = os.path.join(HERE, "_ref", "librkfac_ref_stock.so")  # timed build: the reference's own flags
 
 STATUS_NAMES = {0: "OK", 1: "DimensionMismatch", 2: "RankDeficient", 3: "NoConvergence",
                 4: "DampingNonpositive", 7: "Other"}
@@ -286,6 +287,21 @@ def ref() -> Ref:
 def best() -> Port:
     """The reference build when present, else the restatement."""
     return ref() if ref_available() else port()
+
+
+_ref_stock = None
+
+
+def ref_stock() -> Ref:
+    """The reference compiled with its own flags (proj/CMakeLists.txt:9) -- the CPU baseline that bench.py times."""
+    global _ref_stock
+    if _ref_stock is None:
+        _ref_stock = Ref(REF_STOCK_SO)
+    return _ref_stock
+
+
+def ref_stock_available() -> bool:
+    return os.path.exists(REF_STOCK_SO)
 
 
 def parallel_map(fn, items, threads: int):

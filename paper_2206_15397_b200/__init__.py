@@ -115,6 +115,13 @@ SIGNATURES = {
     "rkfac_plan_set_ea_lo_mode": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_set_max_ctas": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_prepare": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double]),
+    "rkfac_plan_workspace_size": (C.c_size_t, [_vp]),
+    "rkfac_nccl_unique_id": (C.c_int, [_vp]),
+    "rkfac_nccl_init": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    "rkfac_set_nccl_comm": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    "rkfac_allgather": (C.c_int, [_vp, _vp, _vp, _c_i64]),
+    "rkfac_plan_set_gather": (C.c_int, [_vp, _c_i64, C.POINTER(_c_i64), _vp]),
+    "rkfac_plan_gather": (C.c_int, [_vp]),
 }
 
 
@@ -174,6 +181,20 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.rkfac_launch_count(self.h))
 
+    # -- multi-GPU: the NCCL communicator of the one all-gather (rkfac_nccl_init / rkfac_allgather)
+    def nccl_init(self, unique_id: bytes, nranks: int, rank: int):
+        """Joins the clique (blocks until every rank joined); the context owns the communicator."""
+        buf = C.create_string_buffer(bytes(unique_id), len(unique_id))
+        _check(self.lib.rkfac_nccl_init(self.h, C.cast(buf, _vp), nranks, rank), self.h, "nccl_init")
+        self.nranks, self.rank = nranks, rank
+
+    def allgather(self, send, recv):
+        """recv (nranks * send.numel() floats, rank-major) <- every rank's send, on torch's current stream."""
+        self.sync_stream()
+        if recv.numel() != send.numel() * getattr(self, "nranks", 1):
+            raise InvalidArgument("allgather: recv must hold nranks * send.numel() floats")
+        _check(self.lib.rkfac_allgather(self.h, _ptr(send), _ptr(recv), send.numel()), self.h, "allgather")
+
     def __del__(self):
         try:
             self.lib.rkfac_destroy(self.h)
@@ -196,6 +217,15 @@ def context(device: Optional[int] = None) -> Context:
 
 def _ptr(t) -> _vp:
     return _vp(t.data_ptr())
+
+
+def nccl_unique_id() -> bytes:
+    """A new clique's 128-byte ncclUniqueId (rank 0 creates it and ships it to the others, e.g. by
+    torch.distributed.broadcast_object_list)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    _check(lib.rkfac_nccl_unique_id(C.cast(buf, _vp)), None, "nccl_unique_id")
+    return buf.raw
 
 
 def _need_cuda_f32(t, name: str):
@@ -505,6 +535,20 @@ class BatchedStep:
 
     def set_timing(self, on: bool):
         _check(self.ctx.lib.rkfac_plan_set_timing(self.h, 1 if on else 0), self.ctx.h, "set_timing")
+
+    def set_gather(self, chunk: int, offsets: Sequence[int], gathered):
+        """step() ends with the all-gather (rkfac_plan_set_gather): layer l's output packed at offsets[l] of this
+        rank's chunk; every rank's chunk lands in ``gathered`` (nranks * chunk floats).  ``gathered=None`` disables."""
+        offs = (_c_i64 * len(self.layers))(*[int(o) for o in offsets])
+        _check(self.ctx.lib.rkfac_plan_set_gather(self.h, int(chunk), offs, _ptr(gathered) if gathered is not None
+                                                  else None), self.ctx.h, "set_gather")
+
+    def gather(self):
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_gather(self.h), self.ctx.h, "gather")
+
+    def workspace_bytes(self) -> int:
+        return int(self.ctx.lib.rkfac_plan_workspace_size(self.h))
 
     def set_ea_lo_mode(self, mode: int):
         """EA operands' TF32 lo planes: -1 automatic, 0 formed in shared memory, 1 stored by a split pass."""

@@ -3,6 +3,7 @@
 #include <cstring>
 #include <string>
 
+#include "comm.cuh"
 #include "engine.cuh"
 
 using namespace rkfac_b200;
@@ -118,7 +119,50 @@ int rkfac_create(rkfac_context_t* out, int device, void* stream) {
 }
 
 int rkfac_destroy(rkfac_context_t ctx) {
-    return guarded(nullptr, [&] { delete ctx; });
+    return guarded(nullptr, [&] {
+        if (ctx && ctx->c.nccl_owned) nccl_comm_destroy(ctx->c.nccl_comm);
+        delete ctx;
+    });
+}
+
+int rkfac_nccl_unique_id(void* id_out) {
+    return guarded(nullptr, [&] {
+        RKFAC_REQUIRE(id_out, RKFAC_INVALID_ARGUMENT, "null id buffer");
+        nccl_unique_id(id_out);
+    });
+}
+
+int rkfac_nccl_init(rkfac_context_t ctx, const void* unique_id, int nranks, int rank) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && unique_id, RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_CUDA(cudaSetDevice(ctx->c.device));
+        void* comm = nccl_comm_init(unique_id, nranks, rank);
+        if (ctx->c.nccl_owned) nccl_comm_destroy(ctx->c.nccl_comm);
+        ctx->c.nccl_comm = comm;
+        ctx->c.nccl_rank = rank;
+        ctx->c.nccl_nranks = nranks;
+        ctx->c.nccl_owned = true;
+    });
+}
+
+int rkfac_set_nccl_comm(rkfac_context_t ctx, void* nccl_comm, int nranks, int rank) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx, RKFAC_INVALID_ARGUMENT, "null context");
+        RKFAC_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, RKFAC_INVALID_ARGUMENT, "bad NCCL rank / size");
+        if (ctx->c.nccl_owned) nccl_comm_destroy(ctx->c.nccl_comm);
+        ctx->c.nccl_comm = nccl_comm;
+        ctx->c.nccl_rank = rank;
+        ctx->c.nccl_nranks = nranks;
+        ctx->c.nccl_owned = false;
+    });
+}
+
+int rkfac_allgather(rkfac_context_t ctx, const float* send, float* recv, int64_t count) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && (count == 0 || (send && recv)), RKFAC_INVALID_ARGUMENT, "null argument");
+        if (count == 0) return;
+        nccl_allgather(ctx->c.nccl_comm, send, recv, count, ctx->c.stream);
+    });
 }
 
 int rkfac_set_stream(rkfac_context_t ctx, void* stream) {
@@ -139,17 +183,9 @@ int rkfac_ea_update(rkfac_context_t ctx, float* mbar, int64_t ld_mbar, int64_t d
         RKFAC_REQUIRE(m_rows == d, RKFAC_DIMENSION_MISMATCH, "ea_update: update row count != factor dimension");
         RKFAC_REQUIRE(ctx && mbar && (m || n == 0), RKFAC_INVALID_ARGUMENT, "null argument");
         RKFAC_REQUIRE(ld_mbar >= d && ld_m >= n, RKFAC_INVALID_ARGUMENT, "leading dimension too small");
-        GemmBatch b(GemmKind::F32);
-        GemmDesc g = GemmBatch::make((int)d, (int)d, (int)n, m, ld_m, 0, m, ld_m, 1, mbar, ld_mbar, 0);
-        g.sym = 1;
-        g.alpha = (1.0 - rho) * scale * scale;
-        g.beta = rho;
-        g.Cin = mbar;
-        g.ldcin = ld_mbar;
-        b.add(g);
-        b.finalize();
-        b.launch(ctx->c.stream);  // n == 0 gives K = 0: mbar <- rho * mbar
-        RKFAC_CUDA(cudaStreamSynchronize(ctx->c.stream));  // descriptors are freed on return
+        if (d == 0) return;
+        // tcgen05 symmetric SYRK + axpy; stages cached per operand set (single.cu), asynchronous on the stream
+        ctx->c.single.ea_update(mbar, ld_mbar, (int)d, m, ld_m, (int)n, rho, scale, ctx->c.stream);
     });
 }
 
@@ -189,42 +225,20 @@ int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u, int6
         else
             RKFAC_REQUIRE(cols == dim, RKFAC_DIMENSION_MISMATCH, "apply_lowrank_damped_inverse: cols(V) != dim");
         RKFAC_REQUIRE(ctx && u && dvals && v && out && out != v, RKFAC_INVALID_ARGUMENT, "null/aliased argument");
+        RKFAC_REQUIRE(ldu >= r && ldv >= cols && ldo >= cols, RKFAC_INVALID_ARGUMENT, "leading dimension too small");
         Context& c = ctx->c;
-        const size_t wsz = (size_t)r * (side == RKFAC_LEFT ? cols : rows) + (size_t)r;
-        if (c.apply_ws.bytes < wsz * sizeof(float)) c.apply_ws.alloc(wsz * sizeof(float));
-        float* W = c.apply_ws.as<float>();
-        float* br = W + (size_t)r * (side == RKFAC_LEFT ? cols : rows);
-        DevBuf bd;
-        {
-            BracketDesc b{(int)r, dvals, br};
-            bd.alloc(sizeof(BracketDesc));
-            RKFAC_CUDA(cudaMemcpy(bd.p, &b, sizeof(b), cudaMemcpyHostToDevice));
-            launch_bracket(bd.as<BracketDesc>(), 1, lambda, c.stream);
+        if (rows == 0 || cols == 0) return;
+        if (r == 0) {  // no retained modes: out = V / lambda
+            CopyDesc cd{v, out, (int)rows, (int)cols, ldv, ldo, 0};
+            DevBuf b(sizeof(cd));
+            RKFAC_CUDA(cudaMemcpy(b.p, &cd, sizeof(cd), cudaMemcpyHostToDevice));
+            launch_copy(b.as<CopyDesc>(), 1, rows * cols, c.stream);
+            launch_scale(out, ldo, (int)rows, (int)cols, (float)(1.0 / lambda), c.stream);
+            RKFAC_CUDA(cudaStreamSynchronize(c.stream));  // b is freed on return (degenerate case only)
+            return;
         }
-        GemmBatch g1(GemmKind::F32), g2(GemmKind::F32);
-        const double inv = 1.0 / lambda;
-        if (side == RKFAC_LEFT) {
-            // W = diag(bracket) U^T V (r x cols); out = U W + V / lambda   (kfactor.hpp:147-152)
-            GemmDesc a = GemmBatch::make((int)r, (int)cols, (int)dim, u, ldu, 1, v, ldv, 0, W, cols, 0);
-            a.rs = br;
-            g1.add(a);
-            GemmDesc b = GemmBatch::make((int)dim, (int)cols, (int)r, u, ldu, 0, W, cols, 0, out, ldo, 0);
-            b.D = v; b.ldd = ldv; b.gamma = inv;
-            g2.add(b);
-        } else {
-            // W = V U diag(bracket) (rows x r); out = W U^T + V / lambda   (kfactor.hpp:156-160)
-            GemmDesc a = GemmBatch::make((int)rows, (int)r, (int)dim, v, ldv, 0, u, ldu, 0, W, r, 0);
-            a.cs = br;
-            g1.add(a);
-            GemmDesc b = GemmBatch::make((int)rows, (int)dim, (int)r, W, r, 0, u, ldu, 1, out, ldo, 0);
-            b.D = v; b.ldd = ldv; b.gamma = inv;
-            g2.add(b);
-        }
-        g1.finalize();
-        g2.finalize();
-        g1.launch(c.stream);
-        g2.launch(c.stream);
-        RKFAC_CUDA(cudaStreamSynchronize(c.stream));
+        // two tcgen05 GEMMs, bracket scale and +V/lambda fused; stages cached per operand set (single.cu)
+        c.single.apply(u, ldu, dvals, (int)dim, (int)r, lambda, v, ldv, (int)rows, (int)cols, side, out, ldo, c.stream);
     });
 }
 
@@ -318,6 +332,23 @@ int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas) {
         plan->p->set_max_ctas(ctas);
     });
 }
+
+int rkfac_plan_set_gather(rkfac_plan_t plan, int64_t chunk_elems, const int64_t* offsets, float* gathered) {
+    return guarded(plan ? plan->ctx : nullptr, [&] {
+        RKFAC_REQUIRE(plan && (!gathered || offsets), RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_REQUIRE(!gathered || plan->ctx->c.nccl_comm, RKFAC_INVALID_ARGUMENT,
+                      "set_gather: attach an NCCL communicator to the context first (rkfac_nccl_init)");
+        std::vector<long long> off;
+        if (offsets) off.assign(offsets, offsets + plan->p->nlayers());
+        plan->p->set_gather(chunk_elems, off.data(), gathered);
+    });
+}
+
+int rkfac_plan_gather(rkfac_plan_t plan) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->gather(); });
+}
+
+size_t rkfac_plan_workspace_size(rkfac_plan_t plan) { return plan ? plan->p->workspace_bytes() : 0; }
 
 int rkfac_plan_set_ea_lo_mode(rkfac_plan_t plan, int mode) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_ea_lo_mode(mode); });

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "comm.cuh"
 #include "engine.cuh"
 
 namespace rkfac_b200 {
@@ -714,7 +715,41 @@ void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double la
     }
     decompose(1, root, stp, fresh);
     precondition(lambda);
+    if (gathered_) gather();
     mark(kStep, false);
+}
+
+void Plan::set_gather(long long chunk, const long long* offsets, float* gathered) {
+    RKFAC_REQUIRE(!layers_.empty(), RKFAC_INVALID_ARGUMENT, "set_gather: no layers bound");
+    if (!gathered) {
+        gathered_ = nullptr;
+        return;
+    }
+    std::vector<CopyDesc> cp;
+    long long off = 0;
+    for (size_t l = 0; l < layers_.size(); ++l) {
+        const LayerState& L = layers_[l];
+        const int dG = f_[L.g].d, dA = f_[L.a].d;
+        RKFAC_REQUIRE(offsets[l] >= 0 && offsets[l] + (long long)dG * dA <= chunk, RKFAC_INVALID_ARGUMENT,
+                      "set_gather: layer output outside the chunk");
+        // the output is dG x dA contiguous: one row of dG*dA floats into the chunk
+        cp.push_back(CopyDesc{L.out, nullptr, 1, dG * dA, (long long)dG * dA, (long long)dG * dA, off});
+        off += (long long)dG * dA;
+    }
+    gather_send_.alloc(sizeof(float) * (size_t)std::max<long long>(1, chunk));
+    RKFAC_CUDA(cudaMemset(gather_send_.p, 0, sizeof(float) * (size_t)std::max<long long>(1, chunk)));
+    for (size_t l = 0; l < cp.size(); ++l) cp[l].dst = gather_send_.as<float>() + offsets[l];
+    upload(d_pack_, cp);
+    pack_total_ = off;
+    gather_chunk_ = chunk;
+    gathered_ = gathered;
+}
+
+void Plan::gather() {
+    RKFAC_REQUIRE(gathered_, RKFAC_INVALID_ARGUMENT, "gather: set_gather was not called");
+    cudaStream_t s = ctx_->stream;
+    launch_copy(d_pack_.as<CopyDesc>(), (int)layers_.size(), pack_total_, s);
+    nccl_allgather(ctx_->nccl_comm, gather_send_.as<float>(), gathered_, gather_chunk_, s);
 }
 
 }  // namespace rkfac_b200

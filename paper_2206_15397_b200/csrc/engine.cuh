@@ -13,6 +13,7 @@
 #include "dmma.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "single.cuh"
 #include "tc_gemm.cuh"
 
 namespace rkfac_b200 {
@@ -84,6 +85,11 @@ class Plan {
     ~Plan();
 
     int nfactors() const { return (int)f_.size(); }
+    int nlayers() const { return (int)layers_.size(); }
+    // device bytes the plan owns (rkfac_plan_workspace_size): per-factor arena, layer arena, sample lo planes, gather
+    size_t workspace_bytes() const {
+        return arena_.bytes + layer_arena_.bytes + ml_arena_.bytes + gather_send_.bytes;
+    }
     FactorState& factor(int i) { return f_[i]; }
     int method() const { return method_; }
 
@@ -103,6 +109,10 @@ class Plan {
     void decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh = false);
     void precondition(double lambda);
     void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
+    // Multi-GPU (config 4): step() ends with packing this rank's layer outputs at offsets[l] of a chunk of chunk
+    // floats and all-gathering the chunks over the context's NCCL communicator into gathered (nranks * chunk).
+    void set_gather(long long chunk, const long long* offsets, float* gathered);
+    void gather();
     // Builds every stage a step with these parameters uses (descriptor uploads), so that the step itself only
     // enqueues kernels and can be captured into a CUDA graph.
     void prepare(double rho, double scale, double lambda);
@@ -132,6 +142,9 @@ class Plan {
     std::vector<FactorState> f_;
     std::vector<LayerState> layers_;
     DevBuf arena_, layer_arena_, ml_arena_;
+    DevBuf gather_send_, d_pack_;  // packed chunk of this rank's outputs and its copy descriptors
+    float* gathered_ = nullptr;
+    long long gather_chunk_ = 0, pack_total_ = 0;
     bool factors_bound_ = false, samples_bound_ = false;
     bool x_tma_ok_ = true;   // every bound X is a valid TMA operand (else a padded copy is made per decomposition)
     bool samples_tma_ok_ = false;  // every bound sample matrix is a valid TMA operand
@@ -180,7 +193,12 @@ struct Context {
         DevBuf ut, dv;
     };
     std::vector<Cached> cache;
-    DevBuf apply_ws;
+    // cached tcgen05 stages of the single-factor ea_update / apply_lowrank_damped_inverse (single.cu)
+    SingleOps single;
+    // optional NCCL communicator (ncclComm_t, caller-owned) for the plan's all-gather (comm.cu)
+    void* nccl_comm = nullptr;
+    int nccl_rank = 0, nccl_nranks = 1;
+    bool nccl_owned = false;  // created by rkfac_nccl_init: destroyed with the context
 };
 
 bool tc_operand_ok(const float* p, long long ld);

@@ -113,4 +113,7 @@ void launch_copy(const CopyDesc* d_descs, int n, long long total, cudaStream_t s
 // return U in the reference's d x r layout).
 void launch_transpose(const float* in, long long ldi, int rows, int cols, float* out, long long ldo, cudaStream_t s);
 
+// x (rows x cols, pitch ld) *= a (ea_update with an empty update, kfactor.hpp:33-41 with n = 0).
+void launch_scale(float* x, long long ld, int rows, int cols, float a, cudaStream_t s);
+
 }  // namespace rkfac_b200

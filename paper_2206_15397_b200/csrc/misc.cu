@@ -78,18 +78,27 @@ __global__ void bracket_kernel(const BracketDesc* __restrict__ descs, double lam
     }
 }
 
-__global__ void copy_kernel(const CopyDesc* __restrict__ descs, int n, long long total) {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+// One descriptor per blockIdx.y, one row per warp, float4 accesses when both rows are 16-byte aligned.
+__global__ void copy_kernel(const CopyDesc* __restrict__ descs) {
+    const CopyDesc cd = descs[blockIdx.y];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const bool vec = ((reinterpret_cast<uintptr_t>(cd.src) | reinterpret_cast<uintptr_t>(cd.dst) |
+                       (uintptr_t)(cd.lds * 4) | (uintptr_t)(cd.ldd * 4)) & 15) == 0;
+    const int c4 = vec ? cd.cols / 4 : 0;
+    for (int r = blockIdx.x * wpb + warp; r < cd.rows; r += gridDim.x * wpb) {
+        const float* s = cd.src + (long long)r * cd.lds;
+        float* d = cd.dst + (long long)r * cd.ldd;
+        for (int c = lane; c < c4; c += 32)
+            reinterpret_cast<float4*>(d)[c] = reinterpret_cast<const float4*>(s)[c];
+        for (int c = 4 * c4 + lane; c < cd.cols; c += 32) d[c] = s[c];
+    }
+}
+
+__global__ void scale_kernel(float* __restrict__ x, long long ld, int rows, int cols, float a) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
          e += (long long)gridDim.x * blockDim.x) {
-        int lo = 0, hi = n - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (descs[mid].offset <= e) lo = mid; else hi = mid - 1;
-        }
-        const CopyDesc& cd = descs[lo];
-        const long long local = e - cd.offset;
-        const int r = (int)(local / cd.cols), c = (int)(local - (long long)r * cd.cols);
-        cd.dst[(long long)r * cd.ldd + c] = cd.src[(long long)r * cd.lds + c];
+        const long long r = e / cols, c = e - r * cols;
+        x[r * ld + c] *= a;
     }
 }
 
@@ -134,9 +143,18 @@ void launch_bracket(const BracketDesc* d_descs, int n, double lambda, cudaStream
 }
 
 void launch_copy(const CopyDesc* d_descs, int n, long long total, cudaStream_t s) {
-    if (total == 0) return;
-    const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
-    copy_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
+    if (total == 0 || n == 0) return;
+    // ~8 row-blocks of 8 warps per SM over all descriptors; blocks past a descriptor's rows exit at once
+    const int bx = (int)std::max<long long>(1, std::min<long long>(512, ceil_div(kNumSMs * 8, n)));
+    copy_kernel<<<dim3(bx, n), 256, 0, s>>>(d_descs);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+}
+
+void launch_scale(float* x, long long ld, int rows, int cols, float a, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return;
+    const int blocks = (int)std::min<long long>(ceil_div((long long)rows * cols, 256), kNumSMs * 8);
+    scale_kernel<<<blocks, 256, 0, s>>>(x, ld, rows, cols, a);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

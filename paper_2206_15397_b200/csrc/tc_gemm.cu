@@ -829,20 +829,30 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const TcProb* __restrict
     }
 }
 
-__global__ void split_kernel(const SplitDesc* __restrict__ descs, int n, long long total) {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        int lo = 0, hi = n - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (descs[mid].offset <= e) lo = mid; else hi = mid - 1;
+// One descriptor per blockIdx.y, one row per warp, float4 accesses when every row involved is 16-byte aligned.
+__global__ void split_kernel(const SplitDesc* __restrict__ descs) {
+    const SplitDesc sd = descs[blockIdx.y];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const bool vec = ((reinterpret_cast<uintptr_t>(sd.src) | reinterpret_cast<uintptr_t>(sd.hi) |
+                       reinterpret_cast<uintptr_t>(sd.lo) | (uintptr_t)(sd.lds * 4) | (uintptr_t)(sd.ldd * 4)) & 15) == 0;
+    const int c4 = vec ? sd.cols / 4 : 0;
+    for (int r = blockIdx.x * wpb + warp; r < sd.rows; r += gridDim.x * wpb) {
+        const float* s = sd.src + (long long)r * sd.lds;
+        float* h = sd.hi ? sd.hi + (long long)r * sd.ldd : nullptr;
+        float* l = sd.lo ? sd.lo + (long long)r * sd.ldd : nullptr;
+        for (int c = lane; c < c4; c += 32) {
+            const float4 x = reinterpret_cast<const float4*>(s)[c];
+            if (h) reinterpret_cast<float4*>(h)[c] = x;
+            if (l)
+                reinterpret_cast<float4*>(l)[c] =
+                    make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                x.w - tf32_trunc(x.w));
         }
-        const SplitDesc& sd = descs[lo];
-        const long long local = e - sd.offset;
-        const int r = (int)(local / sd.cols), c = (int)(local - (long long)r * sd.cols);
-        const float x = sd.src[(long long)r * sd.lds + c];
-        if (sd.hi) sd.hi[(long long)r * sd.ldd + c] = x;
-        if (sd.lo) sd.lo[(long long)r * sd.ldd + c] = x - tf32_trunc(x);
+        for (int c = 4 * c4 + lane; c < sd.cols; c += 32) {
+            const float x = s[c];
+            if (h) h[c] = x;
+            if (l) l[c] = x - tf32_trunc(x);
+        }
     }
 }
 
@@ -948,10 +958,39 @@ int TcGemm::add(const TcProblemDesc& d) {
             }
     }
     probs_.push_back(p);
+    TcProblemDesc kept = d;
+    kept.ksplit = ks;  // a re-add (finalize's N split) keeps the K slicing, hence the arithmetic
+    descs_.push_back(kept);
     return prob;
 }
 
 void TcGemm::finalize() {
+    // A grid that leaves most SMs idle (a plan with few factors owning its GPU: a multi-GPU shard, a single-factor
+    // call) gets narrower N tiles until its tiles fill at least half the SMs.  Every output element keeps its K order
+    // (the N split only changes which CTA owns it), so the result is bitwise the same as with wide tiles; with a full
+    // grid the wide tiles stay (N tiles of 128 measured 46 % slower at VGG16 scale: the A operand is re-read).
+    // RKFAC_TC_NSPLIT=0 disables.
+    static const bool nsplit_on = [] {
+        const char* e = std::getenv("RKFAC_TC_NSPLIT");
+        return !(e && e[0] == '0');
+    }();
+    if (nsplit_on && cap_ == 0 && std::getenv("RKFAC_TC_MAX_CTAS") == nullptr) {
+        for (int it = 0; it < 4; ++it) {
+            long long units = 0;
+            for (const auto& t : tiles_) units += t.pair ? 2 : 1;
+            if (units * 2 >= kNumSMs) break;
+            std::vector<TcProblemDesc> nd = descs_;
+            bool changed = false;
+            for (size_t i = 0; i < nd.size(); ++i)
+                if (!nd[i].sym && probs_[i].n_tile >= 64) {
+                    nd[i].max_n_tile = (int)ceil_div(probs_[i].n_tile / 2, 16) * 16;
+                    changed = true;
+                }
+            if (!changed) break;
+            probs_.clear(); maps_.clear(); tiles_.clear(); descs_.clear();
+            for (const auto& d : nd) add(d);
+        }
+    }
     // Paired tiles halve the B traffic but also the number of schedulable units: keep them only when the paired
     // units still fill every SM (pairing never changes the arithmetic, so this may depend on the batch).
     {
@@ -1066,9 +1105,10 @@ double TcGemm::flops() const {
 }
 
 void launch_split(const SplitDesc* d_descs, int n, long long total, cudaStream_t s) {
-    if (total == 0) return;
-    const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
-    split_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
+    if (total == 0 || n == 0) return;
+    // ~8 row-blocks of 8 warps per SM over all descriptors; blocks past a descriptor's rows exit at once
+    const int bx = (int)std::max<long long>(1, std::min<long long>(512, ceil_div(kNumSMs * 8, n)));
+    split_kernel<<<dim3(bx, n), 256, 0, s>>>(d_descs);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

@@ -82,6 +82,7 @@ class TcGemm {
 
   private:
     std::vector<TcProb> probs_;
+    std::vector<TcProblemDesc> descs_;  // as added (with the resolved K split), for finalize's N split
     std::vector<CUtensorMap> maps_;
     std::vector<TcTile> tiles_;
     std::vector<size_t> partial_off_;

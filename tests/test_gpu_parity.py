@@ -74,7 +74,8 @@ def test_ea_update_zero_and_no_memory_cases(port, cuda):
     m, _ = port.sample_gaussian(1, 0, 3, 2)
     g = rk.EAKFactor.create(3, 0.0, device=cuda)
     rk.ea_update(g, t32(m, cuda))
-    assert np.abs(np64(g.mbar) - m @ m.T).max() <= 1e-6
+    # 3xTF32 on the tensor cores: relative to the entries (|m m^T| ~ 5 here), ~2^-21 per product
+    assert np.abs(np64(g.mbar) - m @ m.T).max() <= 1e-6 * max(1.0, np.abs(m @ m.T).max())
 
 
 def test_ea_update_dimension_check(cuda):
