@@ -90,6 +90,32 @@ int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u_dev, 
                                        const float* v_dev, int64_t ld_v, int64_t rows, int64_t cols, int side,
                                        float* out_dev, int64_t ld_out);
 
+/* ---- factor statistics of convolution layers -------------------------------------------
+ * The reference's MLP forms A_l = [a_{l-1}; 1] (with_ones_row, network.hpp:94-95) and G_l = delta_l
+ * (network.hpp:134), and accumulate_factors feeds M = X / sqrt(n) to ea_update (network.hpp:155-165).  For a
+ * convolution the statistics run over every output location: A is the patch matrix with a ones row,
+ * d = C*kh*kw + 1 rows, n = B*Ho*Wo columns; G is the output gradient, Co rows, n columns.  Both write the EA operand
+ * M = X * scale directly (row-major, pitch ld_out >= n); pass scale = 1/sqrt(n) and then rkfac_plan_ea_update(rho, 1).
+ * Long n (> 512) is handled by the plan's EA as K slices of 512 + the symmetrize pass (accuracy). */
+/* x: B x C x H x W (NCHW, contiguous); out[(c*kh + ky)*kw + kx][(b*Ho + oy)*Wo + ox]; ones_row appends a row of
+ * `scale`.  Ho = (H + 2 ph - dh (kh-1) - 1) / sh + 1, likewise Wo. */
+int rkfac_conv_patches(rkfac_context_t ctx, const float* x_dev, int64_t batch, int64_t channels, int64_t height,
+                       int64_t width, int64_t kh, int64_t kw, int64_t stride_h, int64_t stride_w, int64_t pad_h,
+                       int64_t pad_w, int64_t dil_h, int64_t dil_w, int ones_row, double scale, float* out_dev,
+                       int64_t ld_out);
+/* dy: B x Co x Ho x Wo (NCHW, contiguous); out[co][b*Ho*Wo + q] = scale * dy[b][co][q]. */
+int rkfac_conv_grads(rkfac_context_t ctx, const float* dy_dev, int64_t batch, int64_t channels, int64_t out_h,
+                     int64_t out_w, double scale, float* out_dev, int64_t ld_out);
+
+/* eig.hpp:210-237 sym_eig: S (n x n symmetric, FP32, pitch lds) = P diag(d) P^T with the eigenvalues descending
+ * (dvals: n FP32, and/or dvals64: n FP64; either may be NULL but not both) and the eigenvectors as the columns of P
+ * (n x n FP32, pitch ldp; NULL: eigenvalues only).  FP64 Householder tridiagonalisation + divide and conquer +
+ * back-transformation on the GPU.  Asymmetry above 1e-4 * max(1, |S|max) -> RKFAC_DIMENSION_MISMATCH
+ * (eig.hpp:213-215's 1e-8 scaled for FP32 storage); no convergence of a leaf QL -> RKFAC_NO_CONVERGENCE.
+ * Synchronous.  The exact K-FAC comparator (kfactor.hpp:165-186) and spectrum (kfactor.hpp:56-63) use it. */
+int rkfac_sym_eig(rkfac_context_t ctx, const float* s_dev, int64_t lds, int64_t n, float* p_dev, int64_t ldp,
+                  float* dvals_dev, double* dvals64_dev);
+
 /* ---- batched plan: every factor of every layer in single launches ------------------------------------ */
 
 typedef struct {

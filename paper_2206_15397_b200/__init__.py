@@ -116,6 +116,9 @@ SIGNATURES = {
     "rkfac_plan_set_max_ctas": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_prepare": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double]),
     "rkfac_plan_workspace_size": (C.c_size_t, [_vp]),
+    "rkfac_sym_eig": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp, _vp]),
+    "rkfac_conv_patches": (C.c_int, [_vp, _vp] + [_c_i64] * 12 + [C.c_int, C.c_double, _vp, _c_i64]),
+    "rkfac_conv_grads": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, C.c_double, _vp, _c_i64]),
     "rkfac_nccl_unique_id": (C.c_int, [_vp]),
     "rkfac_nccl_init": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
     "rkfac_set_nccl_comm": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
@@ -390,22 +393,36 @@ class SymEigResult:  # eig.hpp:20-25: p (n x n, eigenvectors as columns), d (n, 
 
 
 def sym_eig(s, fp64: bool = False) -> SymEigResult:
-    """eig.hpp:210-237 for the exact K-FAC comparator: full symmetric eigendecomposition, eigenvalues descending.
-
-    Not on the rand-K-FAC hot path: this is the cubic baseline the randomized path is measured against
-    (harness.hpp:402-478 bench-inverse), so it uses the CUDA toolkit's dense eigensolver (cuSOLVER syevd through
-    torch.linalg.eigh) instead of a hand-written kernel.  Asymmetry above 1e-8 * max(1, ||S||_max) is rejected like
-    eig.hpp:213-215; the symmetrised matrix is decomposed."""
+    """eig.hpp:210-237 for the exact K-FAC comparator (the cubic baseline of harness.hpp:402-478 bench-inverse) and
+    the spectrum snapshots: full symmetric eigendecomposition, eigenvalues descending, eigenvectors as the columns of
+    ``p``.  This repo's own FP64 solver (csrc/symeig.cu: blocked Householder tridiagonalisation, divide and conquer,
+    WY back-transformation) through ``rkfac_sym_eig``.  Asymmetry above 1e-4 * max(1, ||S||_max) (eig.hpp:213-215's
+    1e-8 scaled for FP32 storage) raises DimensionMismatch; the symmetrised matrix is decomposed.  ``fp64`` is kept
+    for call compatibility: the solver always computes in FP64."""
     torch = _torch()
     _need_cuda_f32(s, "s")
     if s.dim() != 2 or s.shape[0] != s.shape[1]:
         raise DimensionMismatch("sym_eig: matrix must be square")
-    amax = float(s.abs().max()) if s.numel() else 0.0
-    if s.numel() and float((s - s.T).abs().max()) > 1e-8 * max(1.0, amax) * 1e4:  # FP32 storage: 1e4 x the FP64 bar
-        raise DimensionMismatch("sym_eig: matrix is not symmetric")
-    a = 0.5 * (s + s.T)
-    lam, p = torch.linalg.eigh(a.double() if fp64 else a)
-    return SymEigResult(p.flip(1).float().contiguous(), lam.flip(0).float().contiguous())
+    n = s.shape[0]
+    p = torch.empty(n, n, device=s.device, dtype=torch.float32)
+    d = torch.empty(n, device=s.device, dtype=torch.float32)
+    ctx = context(s.device.index)
+    _check(ctx.lib.rkfac_sym_eig(ctx.h, _ptr(s), s.stride(0), n, _ptr(p), p.stride(0), _ptr(d), None), ctx.h,
+           "sym_eig")
+    return SymEigResult(p, d)
+
+
+def sym_eigvals(s):
+    """The eigenvalues alone, descending, in FP64 (kfactor.hpp:56-63 spectrum): the same solver, no P output."""
+    torch = _torch()
+    _need_cuda_f32(s, "s")
+    if s.dim() != 2 or s.shape[0] != s.shape[1]:
+        raise DimensionMismatch("sym_eig: matrix must be square")
+    n = s.shape[0]
+    d = torch.empty(n, device=s.device, dtype=torch.float64)
+    ctx = context(s.device.index)
+    _check(ctx.lib.rkfac_sym_eig(ctx.h, _ptr(s), s.stride(0), n, None, n, None, _ptr(d)), ctx.h, "sym_eig")
+    return d
 
 
 def apply_eig_damped_inverse(eig: SymEigResult, lam: float, v, side: ApplySide):

@@ -242,6 +242,46 @@ int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u, int6
     });
 }
 
+int rkfac_conv_patches(rkfac_context_t ctx, const float* x, int64_t B, int64_t C, int64_t H, int64_t W, int64_t kh,
+                       int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw, int64_t dh, int64_t dw, int ones_row,
+                       double scale, float* out, int64_t ld_out) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && x && out, RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && kh >= 1 && kw >= 1 && sh >= 1 && sw >= 1 && ph >= 0 &&
+                          pw >= 0 && dh >= 1 && dw >= 1,
+                      RKFAC_INVALID_ARGUMENT, "conv_patches: bad geometry");
+        const int64_t Ho = (H + 2 * ph - dh * (kh - 1) - 1) / sh + 1, Wo = (W + 2 * pw - dw * (kw - 1) - 1) / sw + 1;
+        RKFAC_REQUIRE(Ho >= 1 && Wo >= 1, RKFAC_DIMENSION_MISMATCH, "conv_patches: empty output");
+        RKFAC_REQUIRE(ld_out >= B * Ho * Wo, RKFAC_INVALID_ARGUMENT, "conv_patches: ld_out < B*Ho*Wo");
+        ConvPatchDesc p{x, (int)B, (int)C, (int)H, (int)W, (int)kh, (int)kw, (int)sh, (int)sw, (int)ph, (int)pw,
+                        (int)dh, (int)dw, (int)Ho, (int)Wo, ones_row ? 1 : 0, (float)scale, out, ld_out};
+        launch_conv_patches(p, ctx->c.stream);
+    });
+}
+
+int rkfac_conv_grads(rkfac_context_t ctx, const float* dy, int64_t B, int64_t Co, int64_t Ho, int64_t Wo,
+                     double scale, float* out, int64_t ld_out) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && dy && out, RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_REQUIRE(B >= 0 && Co >= 1 && Ho >= 1 && Wo >= 1 && ld_out >= B * Ho * Wo, RKFAC_INVALID_ARGUMENT,
+                      "conv_grads: bad sizes");
+        launch_conv_grads(dy, (int)B, (int)Co, Ho * Wo, (float)scale, out, ld_out, ctx->c.stream);
+    });
+}
+
+int rkfac_sym_eig(rkfac_context_t ctx, const float* s, int64_t lds, int64_t n, float* p, int64_t ldp, float* dvals,
+                  double* dvals64) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && s && (dvals || dvals64), RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_REQUIRE(n >= 1 && lds >= n && (!p || ldp >= n), RKFAC_INVALID_ARGUMENT, "bad sizes");
+        const double asym = ctx->c.symeig.run(s, lds, (int)n, p, ldp, dvals, dvals64, ctx->c.stream);
+        // eig.hpp:213-215 rejects asymmetry above 1e-8 max(1, |S|max) in FP64; FP32 storage rounds at 6e-8, so the
+        // bar is 1e4 times that (an FP32 matrix formed as A B^T without symmetrisation passes, a wrong one does not)
+        RKFAC_REQUIRE(asym <= 1e-4, RKFAC_DIMENSION_MISMATCH, "sym_eig: matrix is not symmetric");
+        RKFAC_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
 int rkfac_plan_create(rkfac_context_t ctx, const rkfac_factor_desc* descs, int n, int method, rkfac_plan_t* out) {
     return guarded(ctx, [&] {
         RKFAC_REQUIRE(ctx && out && (descs || n == 0), RKFAC_INVALID_ARGUMENT, "null argument");

@@ -57,6 +57,8 @@ TcOut out_t(float* p, long long ld) { TcOut o; o.p = p; o.ld = ld; o.t = 1; retu
 // 1.4e-5, orthonormality 1.1e-4 -> 7.8e-6.
 constexpr int kSliceK = 512;
 constexpr int kSliceKFinal = 1024;
+// EA updates with more samples than this (convolution statistics) run as K-sliced products + a symmetrize pass
+constexpr int kEaLongK = 512;
 // The apply's long-K products: at most 8 slices of at least 512 (a slice is one TMEM chain: its length is the
 // latency of the product -- 2048-long slices put ~100 us on a VGG16 group's critical path -- while more slices write
 // more d_G x r partials: 1 GB per layer at d = 16384 with 512-slices)
@@ -465,6 +467,7 @@ void Plan::set_max_ctas(int n) {
 
 void Plan::build_ea_stage(double rho, double scale) {
     ea_tc_stage_.reset();
+    ea_long_stage_.reset();
     ea_simt_.reset();
     std::vector<SplitDesc> sm;
     long long off = 0;
@@ -481,22 +484,41 @@ void Plan::build_ea_stage(double rho, double scale) {
         if (const char* e = std::getenv("RKFAC_EA_STORED_LO")) stored_lo = std::atoi(e) != 0;
         if (ea_lo_mode_ >= 0) stored_lo = ea_lo_mode_ == 1;
         ea_tc_stage_ = new_tc();
+        ea_long_stage_ = new_tc();
+        std::vector<SymDesc> sym;
+        long long sym_off = 0;
         for (auto& F : f_) {
             if (!F.M || F.n == 0) continue;
             TcProblemDesc p;
             p.M = F.d; p.N = F.d; p.K = (int)F.n;
             p.A = F.M; p.A_lo = stored_lo ? F.Ml : nullptr; p.lda = F.ldm;  // default: both lo planes formed in smem
             p.B = F.M; p.B_lo = stored_lo ? F.Ml : nullptr; p.ldb = F.ldm;
-            p.sym = 1;
             p.alpha = (float)((1.0 - rho) * scale * scale);
             p.beta = (float)rho;
             p.Cin = F.X; p.ldcin = F.ldx; p.cin_t = 0;
             p.out0 = out_r(F.X, F.ldx);
-            ea_tc_stage_->add(p);
+            if (F.n <= kEaLongK) {
+                p.sym = 1;  // upper tiles, mirrored: exactly symmetric; one TMEM chain of n <= 512
+                ea_tc_stage_->add(p);
+            } else {
+                // long K (convolution statistics, n = B*H*W): the truncating TMEM accumulation would grow the error
+                // linearly with n (tools/tc_acc.cu), so K is cut into slices of kEaLongK summed in FP32 by the
+                // deterministic split-K reduction, which applies the axpy epilogue; the full square is computed and
+                // symmetrised afterwards, exactly the reference's symmetrize_in_place (kfactor.hpp:39)
+                p.sym = 0;
+                p.slice_k = kEaLongK;
+                ea_long_stage_->add(p);
+                sym.push_back(SymDesc{F.X, F.ldx, F.d, sym_off});
+                sym_off += (long long)F.d * (F.d - 1) / 2;
+            }
             sm.push_back(SplitDesc{F.M, nullptr, F.Ml, F.d, (int)F.n, F.ldm, F.ldm, off});
             off += (long long)F.d * F.n;
         }
         ea_tc_stage_->finalize();
+        ea_long_stage_->finalize();
+        upload(d_sym_, sym);
+        sym_n_ = (int)sym.size();
+        sym_total_ = sym_off;
         if (stored_lo) ea_split_n_ = (int)sm.size();
     } else {
         ea_simt_ = std::make_unique<GemmBatch>(GemmKind::F32);
@@ -618,6 +640,10 @@ void Plan::ea_update(double rho, double scale) {
     if (ea_tc_) {
         if (ea_split_n_ > 0) launch_split(d_split_m_.as<SplitDesc>(), ea_split_n_, split_m_total_, s);
         ea_tc_stage_->launch(s);
+        if (ea_long_stage_ && !ea_long_stage_->empty()) {
+            ea_long_stage_->launch(s);
+            launch_symmetrize(d_sym_.as<SymDesc>(), sym_n_, sym_total_, s);
+        }
     } else {
         ea_simt_->launch(s);
     }

@@ -14,6 +14,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "single.cuh"
+#include "symeig.cuh"
 #include "tc_gemm.cuh"
 
 namespace rkfac_b200 {
@@ -157,7 +158,10 @@ class Plan {
     std::unique_ptr<TcGemm> xq_[2], xq_t_[2], xqf_[2], gram_[2], tri_[2], tri_t_[2], core_[2], lift_[2];
     std::unique_ptr<Gram64Batch> gram64_[2];
     std::unique_ptr<Tri64Batch> tri64_[2];
-    std::unique_ptr<TcGemm> ea_tc_stage_;
+    std::unique_ptr<TcGemm> ea_tc_stage_, ea_long_stage_;
+    DevBuf d_sym_;  // symmetrize descriptors of the long-K EA factors
+    int sym_n_ = 0;
+    long long sym_total_ = 0;
     std::unique_ptr<GemmBatch> ea_simt_;
     std::unique_ptr<TcGemm> ap_[4];
     DevBuf d_omega_, d_chol64_, d_chol32_[2], d_complete_[2], d_eig_, d_post_, d_complete_u_, d_bracket_;
@@ -195,6 +199,8 @@ struct Context {
     std::vector<Cached> cache;
     // cached tcgen05 stages of the single-factor ea_update / apply_lowrank_damped_inverse (single.cu)
     SingleOps single;
+    // full d x d eigensolver of the exact K-FAC comparator and the spectrum snapshots (symeig.cu), workspace kept
+    SymEig symeig;
     // optional NCCL communicator (ncclComm_t, caller-owned) for the plan's all-gather (comm.cu)
     void* nccl_comm = nullptr;
     int nccl_rank = 0, nccl_nranks = 1;

@@ -116,4 +116,27 @@ void launch_transpose(const float* in, long long ldi, int rows, int cols, float*
 // x (rows x cols, pitch ld) *= a (ea_update with an empty update, kfactor.hpp:33-41 with n = 0).
 void launch_scale(float* x, long long ld, int rows, int cols, float a, cudaStream_t s);
 
+// x <- (x + x^T) / 2 for every descriptor's square matrix (kfactor.hpp:39 symmetrize_in_place), one launch.
+struct SymDesc {
+    float* x;
+    long long ld;
+    int d;
+    long long offset;  // prefix of d*(d-1)/2 (strictly-lower pairs) over descriptors
+};
+void launch_symmetrize(const SymDesc* d_descs, int n, long long total, cudaStream_t s);
+
+// Convolution factor statistics (stats.cu): the patch matrix of x (B x C x H x W, NCHW) scaled by `scale`,
+// out[(c*kh + ky)*kw + kx][(b*Ho + oy)*Wo + ox], plus a row of `scale` when `ones`.
+struct ConvPatchDesc {
+    const float* x;
+    int B, C, H, W, kh, kw, sh, sw, ph, pw, dh, dw, Ho, Wo, ones;
+    float scale;
+    float* out;
+    long long ld;
+};
+void launch_conv_patches(const ConvPatchDesc& p, cudaStream_t s);
+// out[co][b*hw + q] = scale * dy[b][co][q] (dy: B x Co x hw).
+void launch_conv_grads(const float* dy, int B, int Co, long long hw, float scale, float* out, long long ld,
+                       cudaStream_t s);
+
 }  // namespace rkfac_b200

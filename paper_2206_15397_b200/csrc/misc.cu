@@ -151,6 +151,37 @@ void launch_copy(const CopyDesc* d_descs, int n, long long total, cudaStream_t s
     RKFAC_CHECK_LAUNCH();
 }
 
+__global__ void symmetrize_kernel(const SymDesc* __restrict__ descs, int n, long long total) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (descs[mid].offset <= e) lo = mid; else hi = mid - 1;
+        }
+        const SymDesc sd = descs[lo];
+        // strictly-lower pair index -> (i, j), i > j: i = floor((1 + sqrt(1 + 8q)) / 2)
+        const long long q = e - sd.offset;
+        long long i = (long long)((1.0 + sqrt(1.0 + 8.0 * (double)q)) * 0.5);
+        while (i * (i - 1) / 2 > q) --i;
+        while ((i + 1) * i / 2 <= q) ++i;
+        const long long j = q - i * (i - 1) / 2;
+        float* a = sd.x + i * sd.ld + j;
+        float* b = sd.x + j * sd.ld + i;
+        const float v = 0.5f * (*a + *b);
+        *a = v;
+        *b = v;
+    }
+}
+
+void launch_symmetrize(const SymDesc* d_descs, int n, long long total, cudaStream_t s) {
+    if (total == 0 || n == 0) return;
+    const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 8);
+    symmetrize_kernel<<<blocks, 256, 0, s>>>(d_descs, n, total);
+    count_launch();
+    RKFAC_CHECK_LAUNCH();
+}
+
 void launch_scale(float* x, long long ld, int rows, int cols, float a, cudaStream_t s) {
     if (rows == 0 || cols == 0) return;
     const int blocks = (int)std::min<long long>(ceil_div((long long)rows * cols, 256), kNumSMs * 8);

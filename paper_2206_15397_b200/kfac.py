@@ -102,6 +102,53 @@ def factor_statistics(activations: Sequence, deltas: Sequence):
     return a_mats, list(deltas)
 
 
+def _pair(v):
+    return (int(v), int(v)) if isinstance(v, int) else (int(v[0]), int(v[1]))
+
+
+def conv_output_size(h: int, w: int, kernel_size, stride=1, padding=0, dilation=1):
+    (kh, kw), (sh, sw), (ph, pw), (dh, dw) = map(_pair, (kernel_size, stride, padding, dilation))
+    return (h + 2 * ph - dh * (kh - 1) - 1) // sh + 1, (w + 2 * pw - dw * (kw - 1) - 1) // sw + 1
+
+
+def conv_factor_statistics(x, dy, kernel_size, stride=1, padding=0, dilation=1, out_a=None, out_g=None):
+    """The EA operands of one convolution layer (the conv analogue of network.hpp:88-95, 134 and 155-165), on the GPU
+    (csrc/stats.cu through rkfac_conv_patches / rkfac_conv_grads):
+
+    * A = patch matrix of x (B x C x H x W) with a ones row: (C*kh*kw + 1) x n, n = B*Ho*Wo;
+    * G = output gradient dy (B x Co x Ho x Wo) as Co x n;
+
+    both already scaled by 1/sqrt(n) (accumulate_factors' M = X / sqrt(n)), so the plan's EA runs with scale 1.
+    ``out_a`` / ``out_g`` (row-major, contiguous) may be the plan's sample buffers (no extra copy)."""
+    import torch
+
+    from . import InvalidArgument, _check, _ptr, context
+
+    for t, nm in ((x, "x"), (dy, "dy")):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.dim() == 4 and t.is_contiguous()):
+            raise InvalidArgument(f"conv_factor_statistics: {nm} must be a contiguous CUDA float32 NCHW tensor")
+    (kh, kw), (sh, sw), (ph, pw), (dh, dw) = map(_pair, (kernel_size, stride, padding, dilation))
+    B, Cin, H, W = x.shape
+    Ho, Wo = conv_output_size(H, W, (kh, kw), (sh, sw), (ph, pw), (dh, dw))
+    if dy.shape[0] != B or dy.shape[2] != Ho or dy.shape[3] != Wo:
+        from . import DimensionMismatch
+
+        raise DimensionMismatch("conv_factor_statistics: dy does not match the convolution's output shape")
+    n = B * Ho * Wo
+    d_a, d_g = Cin * kh * kw + 1, dy.shape[1]
+    a = out_a if out_a is not None else torch.empty(d_a, n, device=x.device)
+    g = out_g if out_g is not None else torch.empty(d_g, n, device=x.device)
+    if tuple(a.shape) != (d_a, n) or tuple(g.shape) != (d_g, n) or a.stride(1) != 1 or g.stride(1) != 1:
+        raise InvalidArgument("conv_factor_statistics: output buffers must be (C*kh*kw+1) x n and Co x n, row-major")
+    scale = 1.0 / math.sqrt(n)
+    ctx = context(x.device.index)
+    _check(ctx.lib.rkfac_conv_patches(ctx.h, _ptr(x), B, Cin, H, W, kh, kw, sh, sw, ph, pw, dh, dw, 1, scale,
+                                      _ptr(a), a.stride(0)), ctx.h, "conv_patches")
+    _check(ctx.lib.rkfac_conv_grads(ctx.h, _ptr(dy), B, d_g, Ho, Wo, scale, _ptr(g), g.stride(0)), ctx.h,
+           "conv_grads")
+    return a, g
+
+
 @dataclass
 class StepTimings:  # optimizer.hpp:92-96 (device time, CUDA events)
     factor_update: float = 0.0
@@ -230,10 +277,11 @@ class SpectrumReport:  # kfactor.hpp:44-54
 
 
 def spectrum(factor) -> SpectrumReport:
-    """kfactor.hpp:56-63 on a device factor: full eigenvalues (FP64 eigensolve of the FP32 factor), clamped at 0."""
-    from . import sym_eig
+    """kfactor.hpp:56-63 on a device factor: full eigenvalues (this repo's FP64 eigensolver, csrc/symeig.cu, on the
+    FP32 factor), clamped at 0."""
+    from . import sym_eigvals
 
-    d = sym_eig(factor.contiguous(), fp64=True).d.double().cpu().tolist()
+    d = sym_eigvals(factor.contiguous()).cpu().tolist()
     ev = [max(0.0, v) for v in d]
     return SpectrumReport(ev, ev[0] if ev else 0.0)
 

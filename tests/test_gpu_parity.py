@@ -232,10 +232,12 @@ def test_apply_diagonal_special_cases(cuda):
     v = torch.arange(1, 7, dtype=torch.float32, device=cuda).reshape(3, 2)
     out = np64(rk.apply_lowrank_damped_inverse(full, lam, v, rk.ApplySide.LEFT))
     expect = np64(v) / (np.array([3.0, 2.0, 1.0])[:, None] + lam)
-    assert np.abs(out - expect).max() <= 1e-6
+    # Eq. 11 forms V/lam + U b U^T V: FP32 (3xTF32) rounding relative to the terms' size, |V|/lam = 24 here
+    bar = 1e-6 * max(1.0, np.abs(np64(v)).max() / lam)
+    assert np.abs(out - expect).max() <= bar
     zero = rk.LowRankEig(torch.eye(3, device=cuda)[:, :2].contiguous(), torch.zeros(2, device=cuda))
     out2 = np64(rk.apply_lowrank_damped_inverse(zero, lam, v, rk.ApplySide.LEFT))
-    assert np.abs(out2 - np64(v) / lam).max() <= 1e-6
+    assert np.abs(out2 - np64(v) / lam).max() <= bar
 
 
 @pytest.mark.parametrize("lam", [1e-3, 1e-1, 1.0, 10.0])
