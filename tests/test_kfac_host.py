@@ -70,3 +70,11 @@ def test_runlog_and_spectrum_csv_schema(tmp_path):
     assert decay_orders([1.0, 0.0], 2) == 300.0 and decay_orders([], 5) == 0.0
     rep = SpectrumReport([4.0, 2.0, 0.5, 0.0], 4.0)
     assert rep.count_above(0.1) == 3
+
+
+def test_conv_output_size_matches_the_convolution_arithmetic():
+    from paper_2206_15397_b200.kfac import conv_output_size
+
+    assert conv_output_size(32, 32, 3, 1, 1) == (32, 32)  # VGG16 3x3, padding 1
+    assert conv_output_size(8, 8, 3, 2, 1) == (4, 4)
+    assert conv_output_size(7, 9, (3, 1), (2, 1), (0, 0), (2, 1)) == (2, 9)
