@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "symeig.cuh"
@@ -41,31 +43,40 @@ constexpr double kEps = 1.1102230246251565e-16;  // 2^-53
 // ------------------------------------------------------------------------------------------- FP64 GEMM
 constexpr int kGT = 64, kGK = 16;
 
-__global__ void __launch_bounds__(256) dgemm_kernel(const DGemmDesc* __restrict__ descs, int nd) {
+// nd == 0: the single problem `one` (passed by value: no descriptor upload)
+__global__ void __launch_bounds__(256) dgemm_kernel(const DGemmDesc* __restrict__ descs, int nd, DGemmDesc one) {
     int lo = 0, hi = nd - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (descs[mid].tile_off <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
     }
-    const DGemmDesc g = descs[lo];
-    const int t = blockIdx.x - g.tile_off;
+    const DGemmDesc g = nd ? descs[lo] : one;
+    int t = blockIdx.x - g.tile_off;
+    int kbeg = 0, kend = g.K, slice = 0;
+    if (g.ksplit > 1) {  // tiles of slice s are [s * tiles_mn, (s + 1) * tiles_mn)
+        const int tiles_mn = ((g.M + kGT - 1) / kGT) * g.tiles_n;
+        slice = t / tiles_mn;
+        t -= slice * tiles_mn;
+        kbeg = slice * g.kchunk;
+        kend = min(g.K, kbeg + g.kchunk);
+    }
     const int i0 = (t / g.tiles_n) * kGT, j0 = (t % g.tiles_n) * kGT;
     __shared__ double As[kGK][kGT + 4], Bs[kGK][kGT + 4];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     double acc[4][4] = {};
     const bool a_kfast = g.csA == 1, b_jfast = g.csB == 1;
-    for (int k0 = 0; k0 < g.K; k0 += kGK) {
+    for (int k0 = kbeg; k0 < kend; k0 += kGK) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int e = tid + 256 * u;
             int i, kk;
             if (a_kfast) { i = e / kGK; kk = e % kGK; } else { i = e % kGT; kk = e / kGT; }
             const int gi = i0 + i, gk = k0 + kk;
-            As[kk][i] = (gi < g.M && gk < g.K) ? g.A[gi * g.rsA + gk * g.csA] : 0.0;
+            As[kk][i] = (gi < g.M && gk < kend) ? g.A[gi * g.rsA + gk * g.csA] : 0.0;
             int j;
             if (b_jfast) { kk = e / kGT; j = e % kGT; } else { kk = e % kGK; j = e / kGK; }
             const int gj = j0 + j, gk2 = k0 + kk;
-            Bs[kk][j] = (gj < g.N && gk2 < g.K) ? g.B[gk2 * g.rsB + gj * g.csB] : 0.0;
+            Bs[kk][j] = (gj < g.N && gk2 < kend) ? g.B[gk2 * g.rsB + gj * g.csB] : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -80,17 +91,45 @@ __global__ void __launch_bounds__(256) dgemm_kernel(const DGemmDesc* __restrict_
         }
         __syncthreads();
     }
+    // epilogue: every C element of the thread loaded first (16 independent loads in flight), then the stores
+    if (g.ksplit > 1) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const int gi = i0 + ty * 4 + p;
-        if (gi >= g.M) continue;
+        for (int p = 0; p < 4; ++p) {
+            const int gi = i0 + ty * 4 + p;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int gj = j0 + tx * 4 + q;
+                if (gi < g.M && gj < g.N) g.partial[((long long)slice * g.M + gi) * g.N + gj] = acc[p][q];
+            }
+        }
+        return;
+    }
+    double cv[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int gj = j0 + tx * 4 + q;
-            if (gj >= g.N) continue;
-            double* c = g.C + (long long)gi * g.ldc + gj;
-            *c = g.beta == 0.0 ? g.alpha * acc[p][q] : fma(g.alpha, acc[p][q], g.beta * *c);
+            const int gi = i0 + ty * 4 + p, gj = j0 + tx * 4 + q;
+            cv[p][q] = (g.beta != 0.0 && gi < g.M && gj < g.N) ? g.C[(long long)gi * g.ldc + gj] : 0.0;
         }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int gi = i0 + ty * 4 + p, gj = j0 + tx * 4 + q;
+            if (gi < g.M && gj < g.N) g.C[(long long)gi * g.ldc + gj] = fma(g.alpha, acc[p][q], g.beta * cv[p][q]);
+        }
+}
+
+// split-K reduction in a fixed slice order: C = alpha * sum_s partial[s] + beta * C
+__global__ void dgemm_reduce_kernel(DGemmDesc g) {
+    const long long mn = (long long)g.M * g.N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mn; e += (long long)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < g.ksplit; ++s) acc += g.partial[s * mn + e];
+        const long long i = e / g.N, j = e - i * g.N;
+        double* c = g.C + i * g.ldc + j;
+        *c = g.beta == 0.0 ? g.alpha * acc : fma(g.alpha, acc, g.beta * *c);
     }
 }
 
@@ -177,114 +216,152 @@ __device__ __forceinline__ double grid_partial_sum(const double* part, int idx, 
 
 // One panel of 32 columns (latrd): reflectors v_j (stored in A below the subdiagonal, implicit 1 at j+1), tau_j,
 // d_j, e_j, and the panel's V, W (n x 32) for the trailing update A -= V W^T + W V^T.
+//
+// Thread tid owns row tid (the grid has >= n threads).  Three grid barriers per column j:
+//   X  the previous column's w correction alpha (w = w_raw + alpha v, from the partials of w_raw . v); own row:
+//      a_r = b_r + alpha c_r (the column updated by the panel's earlier reflectors, b and c prepared in Z), the
+//      previous column's final w; partial |a|^2 below the subdiagonal
+//   Y  the reflector (dlarfg) from |a|^2; y = A22 v with v = scal (a - a_{j+1} e_{j+1}) + e_{j+1}, formed as
+//      scal A22 a + (1 - scal a_{j+1}) A22 e_{j+1} (warp per row, coalesced rows of the full symmetric matrix), so
+//      the matrix-vector product needs no barrier after the reflector; partial W^T a, V^T a
+//   Z  W^T v, V^T v from those; own row: v_r, w_raw = tau (y - V (W^T v) - W (V^T v)), partial w_raw . v; the next
+//      column's b_r, c_r (its panel term t = i split into the raw part and the alpha part)
+enum { kWV = 0, kSS = 1, kDots = 8 };  // part layout: [kDots, kDots+64) = W^T a, V^T a
+
 __global__ void __launch_bounds__(kPanelThreads) sytrd_panel_kernel(PanelArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double red[kPanelThreads / 32];
-    __shared__ double slot;
+    __shared__ double red[2][kPanelThreads / 32];
+    __shared__ double bc[2];
     __shared__ double cwv[2 * kNB];
     __shared__ double accs[kPanelThreads / 32][2 * kNB];
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int T = gridDim.x * blockDim.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + warp, GW = gridDim.x * (blockDim.x >> 5);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int gw = blockIdx.x * nw + warp, GW = gridDim.x * nw;
     const long long lda = a.lda;
-    for (int r = a.k + tid; r < a.n; r += T)
+    const int n = a.n, r = tid;  // the row this thread owns
+    const bool own = r < n;
+    double* pub = a.part + gridDim.x * kPS;  // a_{j+1}, published by its owner
+    double* abuf = a.vbuf;
+    auto cta_reduce = [&](double v, int idx) {
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[0][warp] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[0][w];
+            a.part[blockIdx.x * kPS + idx] = t;
+        }
+        __syncthreads();
+    };
+    auto grid_sum = [&](int idx) {
+        if (warp == 0) {
+            double t = 0.0;
+            for (int b2 = lane; b2 < (int)gridDim.x; b2 += 32) t += a.part[b2 * kPS + idx];
+            for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) bc[0] = t;
+        }
+        __syncthreads();
+        const double t = bc[0];
+        __syncthreads();
+        return t;
+    };
+    if (own && r >= a.k)
         for (int t = 0; t < kNB; ++t) { a.V[r * kNB + t] = 0.0; a.W[r * kNB + t] = 0.0; }
-    grid.sync();
-    double alpha2 = 0.0;  // the previous column's w correction: w_final = w_raw + alpha2 * v
+    // column k has no panel updates: b = A(:, k), c = 0
+    double b_r = (own && r >= a.k) ? a.A[r * lda + a.k] : 0.0, c_r = 0.0;
+    if (threadIdx.x == 0) a.part[blockIdx.x * kPS + kWV] = 0.0;
+    double tau_prev = 0.0;
     for (int i = 0; i < a.nbp; ++i) {
         const int j = a.k + i;
-        // S1: column j updated by the panel's earlier reflectors; the last W column is finalised on the fly
-        double ssq = 0.0;
-        {
-            double wj[kNB], vj[kNB];
-            for (int t = 0; t < i; ++t) {
-                vj[t] = a.V[j * kNB + t];
-                wj[t] = a.W[j * kNB + t] + (t == i - 1 ? alpha2 * vj[t] : 0.0);
-            }
-            for (int r = j + tid; r < a.n; r += T) {
-                double x = a.A[r * lda + j];
-                for (int t = 0; t < i; ++t) {
-                    const double vr = a.V[r * kNB + t];
-                    const double wr = a.W[r * kNB + t] + (t == i - 1 ? alpha2 * vr : 0.0);
-                    x -= vr * wj[t] + wr * vj[t];
-                }
-                a.A[r * lda + j] = x;
-                if (r >= j + 2) ssq += x * x;
-            }
+        grid.sync();  // X
+        const double alpha2 = i > 0 ? -0.5 * tau_prev * grid_sum(kWV) : 0.0;
+        double a_r = 0.0;
+        if (own && r >= j) {
+            a_r = b_r + alpha2 * c_r;
+            if (i > 0) a.W[r * kNB + i - 1] += alpha2 * a.V[r * kNB + i - 1];  // final w of the previous column
+            abuf[r] = a_r;
+            if (r == j) { a.A[r * lda + j] = a_r; a.d[j] = a_r; }
+            if (r == j + 1) pub[0] = a_r;
         }
-        ssq = block_sum(ssq, red);
-        if (threadIdx.x == 0) a.part[blockIdx.x * kPS + 0] = ssq;
-        grid.sync();
-        // S2: the reflector (dlarfg): v = (x - beta e_1) / (alpha - beta), tau = (beta - alpha) / beta
-        const double sigma = grid_partial_sum(a.part, 0, &slot);
-        const double alpha = a.A[(j + 1) * lda + j];
+        cta_reduce((own && r >= j + 2) ? a_r * a_r : 0.0, kSS);
+        grid.sync();  // Y
+        const double ssq = grid_sum(kSS);
+        const double a1 = pub[0];
         double beta, tj, scal;
-        if (sigma == 0.0) { beta = alpha; tj = 0.0; scal = 0.0; }
+        if (ssq <= 0.0) { beta = a1; tj = 0.0; scal = 0.0; }
         else {
-            const double nrm = sqrt(alpha * alpha + sigma);
-            beta = alpha >= 0.0 ? -nrm : nrm;
-            tj = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+            const double nrm = sqrt(a1 * a1 + ssq);
+            beta = a1 >= 0.0 ? -nrm : nrm;
+            tj = (beta - a1) / beta;
+            scal = 1.0 / (a1 - beta);
         }
-        if (tid == 0) { a.tau[j] = tj; a.d[j] = a.A[j * lda + j]; a.e[j] = beta; }
-        for (int r = j + tid; r < a.n; r += T) {
-            if (i > 0) a.W[r * kNB + i - 1] += alpha2 * a.V[r * kNB + i - 1];  // finalise the previous w
-            if (r == j + 1) { a.V[r * kNB + i] = 1.0; a.vbuf[r] = 1.0; }
-            else if (r >= j + 2) {
-                const double v = a.A[r * lda + j] * scal;
-                a.V[r * kNB + i] = v;
-                a.A[r * lda + j] = v;  // reflector storage (rows >= j+2; the 1 at j+1 is implicit)
-                a.vbuf[r] = v;
-            }
-        }
-        grid.sync();
-        // S3: y = A22 v (warp per row, coalesced rows of the full symmetric matrix) and the panel dots W^T v, V^T v
+        if (tid == 0) { a.tau[j] = tj; a.e[j] = beta; }
         {
-            double aw = 0.0, av = 0.0;  // lane t accumulates column t of W^T v and V^T v
-            for (int r = j + 1 + gw; r < a.n; r += GW) {
-                const double* row = a.A + r * lda;
+            const double corr = 1.0 - scal * a1;
+            double aw = 0.0, av = 0.0;  // lane t accumulates column t of W^T a and V^T a
+            for (int rr = j + 1 + gw; rr < n; rr += GW) {
+                const double* row = a.A + rr * lda;
                 double y = 0.0;
-                for (int c = j + 1 + lane; c < a.n; c += 32) y = fma(row[c], a.vbuf[c], y);
+                for (int c = j + 1 + lane; c < n; c += 32) y = fma(row[c], abuf[c], y);
                 for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-                if (lane == 0) a.ybuf[r] = y;
-                const double vr = a.vbuf[r];
-                if (lane < i) { aw = fma(a.W[r * kNB + lane], vr, aw); av = fma(a.V[r * kNB + lane], vr, av); }
+                if (lane == 0) a.ybuf[rr] = scal * y + corr * row[j + 1];
+                const double ar = abuf[rr];
+                if (lane < i) { aw = fma(a.W[rr * kNB + lane], ar, aw); av = fma(a.V[rr * kNB + lane], ar, av); }
             }
             accs[warp][lane] = aw;
             accs[warp][kNB + lane] = av;
             __syncthreads();
             if (threadIdx.x < 2 * kNB) {
-                double s = 0.0;
-                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += accs[w][threadIdx.x];
-                a.part[blockIdx.x * kPS + 1 + threadIdx.x] = s;
+                double sum = 0.0;
+                for (int w = 0; w < nw; ++w) sum += accs[w][threadIdx.x];
+                a.part[blockIdx.x * kPS + kDots + threadIdx.x] = sum;
             }
         }
-        grid.sync();
-        // S4: w = tau (y - V (W^T v) - W (V^T v)); partial w.v
+        grid.sync();  // Z
         if (threadIdx.x < 2 * kNB) {
-            double s = 0.0;
-            if ((threadIdx.x & (kNB - 1)) < i)
-                for (int b = 0; b < (int)gridDim.x; ++b) s += a.part[b * kPS + 1 + threadIdx.x];
-            cwv[threadIdx.x] = s;
+            const int t = threadIdx.x & (kNB - 1);
+            double sum = 0.0;
+            if (t < i) {
+                for (int b2 = 0; b2 < (int)gridDim.x; ++b2) sum += a.part[b2 * kPS + kDots + threadIdx.x];
+                // W^T v = W(j+1,:) + scal (W^T a - W(j+1,:) a_{j+1})   (v_{j+1} = 1, v_r = scal a_r below)
+                const double wj = threadIdx.x < kNB ? a.W[(j + 1) * kNB + t] : a.V[(j + 1) * kNB + t];
+                sum = wj + scal * (sum - wj * a1);
+            }
+            cwv[threadIdx.x] = sum;
         }
         __syncthreads();
-        double wv = 0.0;
-        for (int r = j + 1 + tid; r < a.n; r += T) {
-            double y = a.ybuf[r];
-            for (int t = 0; t < i; ++t) y -= a.V[r * kNB + t] * cwv[t] + a.W[r * kNB + t] * cwv[kNB + t];
-            const double w = tj * y;
-            a.W[r * kNB + i] = w;
-            wv += w * a.vbuf[r];
+        auto w_raw_of = [&](int row) {
+            double y = a.ybuf[row];
+            for (int t = 0; t < i; ++t) y -= a.V[row * kNB + t] * cwv[t] + a.W[row * kNB + t] * cwv[kNB + t];
+            return tj * y;
+        };
+        double wv = 0.0, wr = 0.0, v_r = 0.0;
+        if (own && r >= j + 1) {
+            v_r = (r == j + 1) ? 1.0 : scal * a_r;
+            a.V[r * kNB + i] = v_r;
+            if (r >= j + 2) a.A[r * lda + j] = v_r;  // reflector storage (the 1 at j+1 is implicit)
+            wr = w_raw_of(r);
+            a.W[r * kNB + i] = wr;
+            wv = wr * v_r;
         }
-        wv = block_sum(wv, red);
-        if (threadIdx.x == 0) a.part[blockIdx.x * kPS + 65] = wv;
-        grid.sync();
-        alpha2 = -0.5 * tj * grid_partial_sum(a.part, 65, &slot);
+        if (i + 1 < a.nbp && own && r >= j + 1) {
+            // next column j+1: a_r = b_r + alpha c_r, its panel term t = i split into the raw and the alpha part
+            const int jn = j + 1;
+            const double wj1 = w_raw_of(jn);  // row j+1's raw w (its owner computes the same value)
+            double x = a.A[r * lda + jn];
+            for (int t = 0; t < i; ++t)
+                x -= a.V[r * kNB + t] * a.W[jn * kNB + t] + a.W[r * kNB + t] * a.V[jn * kNB + t];
+            x -= v_r * wj1 + wr;  // V(j+1, i) = 1
+            b_r = x;
+            c_r = -2.0 * v_r;
+        }
+        cta_reduce(wv, kWV);
+        tau_prev = tj;
     }
-    // finalise the last w column
+    grid.sync();
+    const double alpha2 = -0.5 * tau_prev * grid_sum(kWV);
     const int jl = a.k + a.nbp - 1;
-    for (int r = jl + 1 + tid; r < a.n; r += T) a.W[r * kNB + a.nbp - 1] += alpha2 * a.V[r * kNB + a.nbp - 1];
+    if (own && r >= jl + 1) a.W[r * kNB + a.nbp - 1] += alpha2 * a.V[r * kNB + a.nbp - 1];  // last w column
 }
 
 __global__ void last_diag_kernel(const double* A, long long lda, int n, double* d, double* e) {
@@ -527,14 +604,24 @@ __device__ __forceinline__ int find_merge(const MergeDesc* md, int nm, int gidx)
 
 // M2 (thread per block row r = eigenvector component): gather the sorted columns, apply the rotations in order,
 // write the nondeflated eigenvectors to QT rows s..s+k-1 and the deflated ones to rows s+k.. (eigenvector-major).
-__global__ void merge_gather_kernel(const MergeDesc* md, int nm, double* QT, double* QgT, long long ldq, DcArrays w) {
+__global__ void merge_gather_kernel(const MergeDesc* md, int nm, double* __restrict__ QT, double* __restrict__ QgT,
+                                    long long ldq, DcArrays w) {
     const int gidx = blockIdx.x * blockDim.x + threadIdx.x;  // global component index
     const int mi = find_merge(md, nm, gidx);
     const MergeDesc g = md[mi];
     if (gidx >= g.s + g.m) return;
     const int s = g.s, m = g.m, r = gidx - s;
     const MergeMeta mt = w.meta[mi];
-    for (int idx = 0; idx < m; ++idx) QgT[(long long)(s + idx) * ldq + s + r] = QT[(long long)(s + w.perm[s + idx]) * ldq + s + r];
+    constexpr int U = 8;  // loads in flight per thread
+    for (int i0 = 0; i0 < m; i0 += U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            v[u] = i0 + u < m ? QT[(long long)(s + w.perm[s + i0 + u]) * ldq + s + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u < m) QgT[(long long)(s + i0 + u) * ldq + s + r] = v[u];
+    }
     for (int q = 0; q < mt.nrot; ++q) {
         const int p = w.rp[s + q], qq = w.rq[s + q];
         const double c = w.rc[s + q], sn = w.rs[s + q];
@@ -544,12 +631,27 @@ __global__ void merge_gather_kernel(const MergeDesc* md, int nm, double* QT, dou
         *xp = c * x + sn * y;
         *xq = c * y - sn * x;
     }
-    for (int a = 0; a < mt.k; ++a) QT[(long long)(s + a) * ldq + s + r] = QgT[(long long)(s + w.ndidx[s + a]) * ldq + s + r];
-    for (int b = 0; b < mt.kd; ++b)
-        QT[(long long)(s + mt.k + b) * ldq + s + r] = QgT[(long long)(s + w.dfidx[s + b]) * ldq + s + r];
+    const int k = mt.k, kd = mt.kd;
+    for (int i0 = 0; i0 < k + kd; i0 += U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = i0 + u;
+            v[u] = e < k + kd ? QgT[(long long)(s + (e < k ? w.ndidx[s + e] : w.dfidx[s + e - k])) * ldq + s + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u < k + kd) QT[(long long)(s + i0 + u) * ldq + s + r] = v[u];
+    }
 }
 
-// M3 (warp per root): the secular equation by bisection on the offset from the nearer pole.
+// M3 (warp per root): the secular equation f(lambda) = 1/rho + sum z_i^2 / (d_i - lambda) = 0 (f/rho: same sign),
+// lambda = d_org + tau with org the nearer pole, so every d_i - lambda = (d_i - d_org) - tau is formed without
+// cancellation.  A bracket [lo, hi] (f(lo) < 0 <= f(hi); f increases) is kept; each iteration takes the root of the
+// two-pole rational model of f at the current point (psi and phi -- the sums over the poles left and right of the
+// root -- each matched in value and slope by a constant plus one pole: the classic scheme behind LAPACK's dlaed4),
+// falling back to bisection whenever the model's root leaves the bracket.  Converges in a handful of iterations;
+// the bracket alone bounds the worst case.
 __global__ void secular_kernel(const MergeDesc* md, int nm, DcArrays w, int total) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= total) return;
@@ -560,35 +662,72 @@ __global__ void secular_kernel(const MergeDesc* md, int nm, DcArrays w, int tota
     if (j >= k) return;
     const double* dn = w.dnd + s;
     const double* zn = w.znd + s;
-    const double rho = mt.rhon;
-    // f(org, tau) = 1 + rho sum z_i^2 / ((d_i - d_org) - tau)
-    auto f = [&](int o, double t) {
-        double acc = 0.0;
+    const double irho = 1.0 / mt.rhon;
+    // sums at offset t from pole o: psi (i <= j), dpsi, phi (i > j), dphi
+    auto sums = [&](int o, double t, double& psi, double& dpsi, double& phi, double& dphi) {
+        psi = dpsi = phi = dphi = 0.0;
         const double dor = dn[o];
-        for (int i = lane; i < k; i += 32) acc += zn[i] * zn[i] / ((dn[i] - dor) - t);
-        for (int q = 16; q; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
-        return 1.0 + rho * acc;
+        for (int i = lane; i < k; i += 32) {
+            const double r = 1.0 / ((dn[i] - dor) - t);
+            const double q = zn[i] * zn[i] * r;
+            if (i <= j) { psi += q; dpsi += q * r; } else { phi += q; dphi += q * r; }
+        }
+        for (int q = 16; q; q >>= 1) {
+            psi += __shfl_xor_sync(0xffffffffu, psi, q);
+            dpsi += __shfl_xor_sync(0xffffffffu, dpsi, q);
+            phi += __shfl_xor_sync(0xffffffffu, phi, q);
+            dphi += __shfl_xor_sync(0xffffffffu, dphi, q);
+        }
     };
+    double psi, dpsi, phi, dphi;
     int o;
-    double lo, hi;
+    double lo, hi, t;
     if (j < k - 1) {
         const double half = 0.5 * (dn[j + 1] - dn[j]);
-        if (f(j, half) >= 0.0) { o = j; lo = 0.0; hi = half; }        // root in (d_j, midpoint]
-        else { o = j + 1; lo = -half; hi = 0.0; }                       // root in (midpoint, d_{j+1})
+        sums(j, half, psi, dpsi, phi, dphi);
+        if (irho + psi + phi >= 0.0) { o = j; lo = 0.0; hi = half; }  // root in (d_j, midpoint]
+        else { o = j + 1; lo = -half; hi = 0.0; }                      // root in (midpoint, d_{j+1})
     } else {
         double zz = 0.0;
         for (int i = lane; i < k; i += 32) zz += zn[i] * zn[i];
         for (int q = 16; q; q >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, q);
-        o = j; lo = 0.0; hi = rho * zz;
+        o = j; lo = 0.0; hi = zz / irho;
     }
-    // invariant: f(lo) < 0 <= f(hi) (f increases on the interval); lo/hi never touch the pole itself
-    for (int it = 0; it < 200; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        if (mid == lo || mid == hi || hi - lo <= 2.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
-        if (f(o, mid) >= 0.0) hi = mid; else lo = mid;
+    t = 0.5 * (lo + hi);
+    for (int it = 0; it < 100; ++it) {
+        sums(o, t, psi, dpsi, phi, dphi);
+        const double f = irho + psi + phi;
+        if (f < 0.0) lo = t; else hi = t;
+        if (f == 0.0 || hi - lo <= 2.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
+        // two-pole model around the poles j (left) and j+1 (right) of the root
+        const double dj = (dn[j] - dn[o]) - t;
+        double tn;
+        if (j < k - 1) {
+            const double dj1 = (dn[j + 1] - dn[o]) - t;
+            const double sl = dpsi * dj * dj, sr = dphi * dj1 * dj1;
+            const double c = f - dpsi * dj - dphi * dj1;
+            // c eta^2 - B eta + C = 0, eta the move of lambda
+            const double B = c * (dj + dj1) + sl + sr, C = c * dj * dj1 + sl * dj1 + sr * dj;
+            const double disc = fmax(0.0, B * B - 4.0 * c * C);
+            double e1, e2;
+            if (c == 0.0) { e1 = e2 = C / B; }
+            else {
+                const double qq = 0.5 * (B + copysign(sqrt(disc), B));
+                e1 = qq / c;
+                e2 = qq != 0.0 ? C / qq : e1;
+            }
+            const double t1 = t + e1, t2 = t + e2;
+            tn = (t1 > lo && t1 < hi) ? t1 : ((t2 > lo && t2 < hi) ? t2 : 0.5 * (lo + hi));
+        } else {
+            const double sl = dpsi * dj * dj;
+            const double c = f - dpsi * dj;  // c + sl / (dj - eta) = 0
+            tn = c != 0.0 ? t + dj + sl / c : 0.5 * (lo + hi);
+            if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+        }
+        if (fabs(tn - t) <= 2.0 * kEps * fabs(t)) { t = tn; break; }
+        t = tn;
     }
     if (lane == 0) {
-        const double t = 0.5 * (lo + hi);
         w.org[s + j] = o;
         w.tau[s + j] = (t == 0.0) ? (o == j ? hi : lo) : t;
     }
@@ -697,15 +836,15 @@ __global__ void build_v_kernel(const double* A, long long lda, int n, int k, int
 
 // T (32 x 32 upper triangular, row-major): T(t,t) = tau_t, T(0:t, t) = -tau_t T(0:t, 0:t) G(0:t, t), G = V^T V.
 __global__ void build_t_kernel(const double* G, const double* tau, int k, int nbp, double* T) {
-    __shared__ double Ts[kNB][kNB + 1];
+    __shared__ double Ts[kNB][kNB + 1], Gs[kNB][kNB + 1];
     const int lane = threadIdx.x;
-    for (int r = 0; r < kNB; ++r) Ts[r][lane] = 0.0;
+    for (int r = 0; r < kNB; ++r) { Ts[r][lane] = 0.0; Gs[r][lane] = G[r * kNB + lane]; }
     __syncwarp();
     for (int t = 0; t < nbp; ++t) {
         const double tt = tau[k + t];
         double acc = 0.0;
         if (lane < t)
-            for (int c = lane; c < t; ++c) acc += Ts[lane][c] * G[c * kNB + t];
+            for (int c = lane; c < t; ++c) acc += Ts[lane][c] * Gs[c][t];
         __syncwarp();
         if (lane < t) Ts[lane][t] = -tt * acc;
         if (lane == 0) Ts[t][t] = tt;
@@ -729,13 +868,38 @@ void DGemmBatch::add(DGemmDesc d) {
 
 void DGemmBatch::launch(cudaStream_t s) {
     if (descs_.empty()) return;
+    if (descs_.size() == 1) {  // by value: fully asynchronous
+        DGemmDesc g = descs_[0];
+        const int tiles_mn = (int)ceil_div(g.M, kGT) * g.tiles_n;
+        // few output tiles and a long K (the skinny products of the back-transformation): split K
+        if (tiles_mn < 2 * kNumSMs && g.K >= 512) {
+            const int ks = (int)std::min<long long>(ceil_div(g.K, 256), ceil_div(4 * kNumSMs, tiles_mn));
+            if (ks > 1) {
+                g.ksplit = ks;
+                g.kchunk = (int)(ceil_div(ceil_div(g.K, ks), kGK) * kGK);
+                g.ksplit = (int)ceil_div(g.K, g.kchunk);
+                const size_t bytes = sizeof(double) * (size_t)g.ksplit * g.M * g.N;
+                if (part_.bytes < bytes) part_.alloc(bytes);
+                g.partial = part_.as<double>();
+            }
+        }
+        dgemm_kernel<<<tiles_mn * g.ksplit, 256, 0, s>>>(nullptr, 0, g);
+        count_launch();
+        if (g.ksplit > 1) {
+            dgemm_reduce_kernel<<<(int)std::min<long long>(ceil_div((long long)g.M * g.N, 256), 1184), 256, 0, s>>>(g);
+            count_launch();
+        }
+        check_launch();
+        clear();
+        return;
+    }
     const size_t bytes = sizeof(DGemmDesc) * descs_.size();
     if (cap_ < bytes) {
         d_.alloc(std::max<size_t>(bytes, 4096));
         cap_ = d_.bytes;
     }
     RKFAC_CUDA(cudaMemcpyAsync(d_.p, descs_.data(), bytes, cudaMemcpyHostToDevice, s));
-    dgemm_kernel<<<tiles_, 256, 0, s>>>(d_.as<DGemmDesc>(), (int)descs_.size());
+    dgemm_kernel<<<tiles_, 256, 0, s>>>(d_.as<DGemmDesc>(), (int)descs_.size(), descs_[0]);
     count_launch();
     check_launch();
     // the host vector is the source of an async copy: keep it until the copy is done
@@ -760,7 +924,7 @@ void SymEig::reserve(int n) {
     ev_.alloc(sizeof(double) * (n + 1));
     vbuf_.alloc(sizeof(double) * (n + 1));
     ybuf_.alloc(sizeof(double) * (n + 1));
-    part_.alloc(sizeof(double) * kNumSMs * kPS);
+    part_.alloc(sizeof(double) * (kNumSMs + 1) * kPS);
     ws_.alloc(sizeof(double) * (size_t)(n + 1) * 24 + sizeof(MergeMeta) * (n + 1) + 4096);
     meta_.alloc(sizeof(double) * 4096);
     stat_.alloc(64);
@@ -769,7 +933,10 @@ void SymEig::reserve(int n) {
 void SymEig::tridiagonalize(cudaStream_t s) {
     const int n = n_;
     double* A = A_.as<double>();
-    const int grid = kNumSMs;
+    int grid = (int)std::min<long long>(kNumSMs, std::max(ceil_div(n, kPanelThreads), ceil_div(n, 32)));
+    if (const char* e = std::getenv("RKFAC_SYMEIG_GRID")) grid = std::max<int>((int)ceil_div(n, kPanelThreads), std::atoi(e));
+    RKFAC_REQUIRE((long long)grid * kPanelThreads >= n, RKFAC_INVALID_ARGUMENT,
+                  "sym_eig: n above the panel kernel's row capacity (37888)");
     for (int k = 0; k < n - 1; k += kNB) {
         const int nbp = std::min(kNB, n - 1 - k);
         PanelArgs a{A, ld_, n, k, nbp, V_.as<double>(), W_.as<double>(), tau_.as<double>(), dv_.as<double>(),
@@ -958,17 +1125,34 @@ double SymEig::run(const float* S, long long lds, int n, float* P, long long ldp
     std::memcpy(&asym, &st[1], 8);
     std::memcpy(&amax, &st[2], 8);
     const double rel = asym / std::max(1.0, amax);
+    // RKFAC_SYMEIG_TIMING=1: phase times (CUDA events) to stderr
+    static const bool timing = std::getenv("RKFAC_SYMEIG_TIMING") != nullptr;
+    cudaEvent_t ev[4] = {};
+    if (timing)
+        for (auto& e : ev) { RKFAC_CUDA(cudaEventCreate(&e)); }
+    if (timing) RKFAC_CUDA(cudaEventRecord(ev[0], s));
     if (n > 1) tridiagonalize(s);
     else {
         RKFAC_CUDA(cudaMemcpyAsync(dv_.p, A_.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
         RKFAC_CUDA(cudaMemsetAsync(ev_.p, 0, sizeof(double), s));
     }
+    if (timing) RKFAC_CUDA(cudaEventRecord(ev[1], s));
     divide_and_conquer(s, true);
+    if (timing) RKFAC_CUDA(cudaEventRecord(ev[2], s));
     int fail = 0;
     RKFAC_CUDA(cudaMemcpyAsync(&fail, stat_.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     RKFAC_CUDA(cudaStreamSynchronize(s));
     RKFAC_REQUIRE(!fail, RKFAC_NO_CONVERGENCE, "sym_eig: QL iteration did not converge (eig.hpp:147-148)");
     if (n > 1) back_transform(s);
+    if (timing) {
+        RKFAC_CUDA(cudaEventRecord(ev[3], s));
+        RKFAC_CUDA(cudaEventSynchronize(ev[3]));
+        float t[3];
+        for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+        std::fprintf(stderr, "symeig n=%d: tridiagonalisation %.2f ms, divide and conquer %.2f ms, back-transformation "
+                     "%.2f ms\n", n, t[0], t[1], t[2]);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
     output_kernel<<<grid, dim3(32, 8), 0, s>>>(QT_.as<double>(), ld_, dv_.as<double>(), n, P, ldp, dvals, dvals64);
     count_launch();

@@ -16,6 +16,8 @@ struct DGemmDesc {
     double* C; long long ldc;
     double alpha, beta;
     int tiles_n, tile_off;
+    int ksplit = 1, kchunk = 0;  // split-K (single-problem launches with few tiles): partial sums + reduction
+    double* partial = nullptr;
 };
 
 class DGemmBatch {
@@ -28,7 +30,7 @@ class DGemmBatch {
   private:
     std::vector<DGemmDesc> descs_;
     int tiles_ = 0;
-    DevBuf d_;
+    DevBuf d_, part_;
     size_t cap_ = 0;
 };
 

@@ -64,8 +64,9 @@ def main():
         sxx = sum(x * x for x in xs)
         sxy = sum(x * y for x, y in zip(xs, ys))
         slopes[name] = (n * sxy - sx * sy) / (n * sxx - sx * sx) if n > 1 else None
-    print(json.dumps({"what": "bench-inverse on one B200 (harness.hpp:402-478 construction; exact = cuSOLVER syevd "
-                      "FP32 + our apply kernels; rsvd/srevd = our rand-EVD + apply)", "lambda": lam,
+    print(json.dumps({"what": "bench-inverse on one B200 (harness.hpp:402-478 construction; exact = this repo's FP64 "
+                      "eigensolver csrc/symeig.cu (Householder + divide and conquer) + our apply kernels; rsvd/srevd = "
+                      "our rand-EVD + apply)", "lambda": lam,
                       "sketch": [220, 10, 4], "median_seconds": med, "loglog_slopes": slopes}))
 
 
