@@ -464,17 +464,24 @@ def run_ours(args, wl):
 
     send = torch.zeros(layout.chunk, dtype=torch.float32, device=dev)
     recv = torch.empty(world * layout.chunk, dtype=torch.float32, device=dev)
+    if world > 1:
+        # the collective runs through the C-ABI (rkfac_nccl_init / rkfac_allgather): torch.distributed only ships the
+        # NCCL unique id and does the barriers / max-over-ranks timing
+        uid = [rk.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], world, rank)
 
     graph = None  # CUDA graph of the whole step (rk.StepGraph), captured after the eager warm-up
 
     def gather():
-        """The one collective: pack this rank's preconditioned gradients and all-gather them.  On one
-        GPU every layer's result is already in place, so there is nothing to move."""
+        """The one collective: pack this rank's preconditioned gradients and all-gather them over
+        NVLink/NVSwitch (ncclAllGather through rkfac_allgather).  On one GPU every layer's result is already in place,
+        so there is nothing to move."""
         if world == 1:
             return
         for i, l in enumerate(mine):
             send[layout.offsets[l]:layout.offsets[l] + sizes[l]].copy_(step.outs[i].view(-1))
-        dist.all_gather_into_tensor(recv, send)
+        ctx.allgather(send, recv)
 
     def one_step():
         if graph is not None:
