@@ -83,6 +83,14 @@ int rkfac_rsvd_psd(rkfac_context_t ctx, const float* x_dev, int64_t ld_x, int64_
                    int64_t q, uint64_t seed, uint64_t* counter, float* u_dev, int64_t ld_u, float* dvals_dev,
                    int64_t* rank_out);
 
+/* rnla.hpp:62-77 rsvd on a general x (rows x cols): SvdResult {u: rows x rank_out (ld_u), s: rank_out (descending),
+ * v: cols x rank_out (ld_v)}.  Sketch clamping with dim = min(rows, cols) (rnla.hpp:63); Omega (cols x w) is drawn
+ * from (seed, *counter), which advances by 2*cols*w.  Synchronous; not on the optimizer path (which uses the square
+ * PSD specialisation rkfac_rsvd_psd). */
+int rkfac_rsvd(rkfac_context_t ctx, const float* x_dev, int64_t ld_x, int64_t rows, int64_t cols, int64_t r,
+               int64_t p, int64_t q, uint64_t seed, uint64_t* counter, float* u_dev, int64_t ld_u, float* s_dev,
+               float* v_dev, int64_t ld_v, int64_t* rank_out);
+
 /* kfactor.hpp:134-161.  u: dim x r (row-major, orthonormal columns), dvals: r.  LEFT needs rows == dim,
  * RIGHT needs cols == dim.  lambda <= 0 -> RKFAC_DAMPING_NONPOSITIVE.  out may not alias v. */
 int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u_dev, int64_t ld_u,

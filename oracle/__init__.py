@@ -199,6 +199,8 @@ class Ref(Port):
                          C.c_uint64, _u64p, _dp, _dp, _szp)
         self._apply = L.fn("apply_lowrank", C.c_int, _dp, _dp, C.c_size_t, C.c_size_t, C.c_double, _dp,
                            C.c_size_t, C.c_size_t, C.c_int, _dp)
+        self._rsvd = L.fn("rsvd", C.c_int, _dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
+                          C.c_uint64, _u64p, _dp, _dp, _dp, _szp)
         self._step = L.fn("step_threaded", C.c_int, C.c_int, C.c_int, C.c_size_t, _szp, _szp,
                           C.POINTER(_dp), C.POINTER(_dp), _szp, C.c_double, C.c_size_t, C.c_size_t, C.c_size_t,
                           C.c_uint64, C.c_uint64, C.c_double, C.POINTER(_dp), C.POINTER(_dp), _dp,
@@ -233,6 +235,20 @@ class Ref(Port):
 
     def rsvd_psd(self, x, r, p, q, seed, counter=0):
         return self._decomp_m(1, "rsvd_psd", x, r, p, q, seed, counter)
+
+    def rsvd(self, x, r, p, q, seed, counter=0):
+        """rnla.hpp:62-77 on a general matrix: (u, s, v, counter)."""
+        x = _f64(x)
+        rows, cols = x.shape
+        k = max(1, min(r, rows, cols))
+        u = np.empty((rows, k)); s = np.empty(k); v = np.empty((cols, k))
+        ctr = C.c_uint64(counter); rout = C.c_size_t(0)
+        st = self._rsvd(_ptr(x), rows, cols, r, p, q, seed, C.byref(ctr), _ptr(u), _ptr(s), _ptr(v), C.byref(rout))
+        if st:
+            raise OracleError(st, "rsvd")
+        rr = rout.value
+        return (np.ascontiguousarray(u.reshape(-1)[: rows * rr].reshape(rows, rr)), s[:rr].copy(),
+                np.ascontiguousarray(v.reshape(-1)[: cols * rr].reshape(cols, rr)), int(ctr.value))
 
     def apply_eig_damped_inverse(self, *a, **k):
         return self._port.apply_eig_damped_inverse(*a, **k)

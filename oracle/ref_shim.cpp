@@ -106,6 +106,22 @@ int ref_decompose(int method, const double* x, std::size_t d, std::size_t r, std
     });
 }
 
+// rnla.hpp:62-77 rsvd on a general rows x cols matrix: u (rows x r), s (r), v (cols x r), row-major.
+int ref_rsvd(const double* x, std::size_t rows, std::size_t cols, std::size_t r, std::size_t p, std::size_t q,
+             std::uint64_t seed, std::uint64_t* counter, double* u, double* s, double* v, std::size_t* r_out) {
+    return guarded([&] {
+        RngState rng(seed);
+        rng.counter = *counter;
+        const SketchParams sk{r, p, q};
+        SvdResult res = rsvd(to_mat(x, rows, cols), sk, rng);
+        std::memcpy(u, res.u.data(), sizeof(double) * res.u.size());
+        std::copy(res.s.begin(), res.s.end(), s);
+        std::memcpy(v, res.v.data(), sizeof(double) * res.v.size());
+        *r_out = res.s.size();
+        *counter = rng.counter;
+    });
+}
+
 // side 0 = LEFT, 1 = RIGHT (kfactor.hpp:134).
 int ref_apply_lowrank(const double* u, const double* dv, std::size_t dim, std::size_t r, double lambda,
                       const double* v, std::size_t rows, std::size_t cols, int side, double* out) {

@@ -117,6 +117,8 @@ SIGNATURES = {
     "rkfac_plan_prepare": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double]),
     "rkfac_plan_workspace_size": (C.c_size_t, [_vp]),
     "rkfac_sym_eig": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp, _vp]),
+    "rkfac_rsvd": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, C.POINTER(_c_u64),
+                             _vp, _c_i64, _vp, _vp, _c_i64, C.POINTER(_c_i64)]),
     "rkfac_conv_patches": (C.c_int, [_vp, _vp] + [_c_i64] * 12 + [C.c_int, C.c_double, _vp, _c_i64]),
     "rkfac_conv_grads": (C.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, C.c_double, _vp, _c_i64]),
     "rkfac_nccl_unique_id": (C.c_int, [_vp]),
@@ -355,6 +357,34 @@ def _decompose(fn_name: str, method: DecompMethod, x, params: SketchParams, rng:
     rng.counter = int(ctr.value)
     rr = int(rank.value)
     return LowRankEig(u[:, :rr], dv[:rr], method)
+
+
+@dataclass
+class SvdResult:  # eig.hpp:239-241 / rnla.hpp:62-77: u (rows x r), s (r, descending), v (cols x r)
+    u: object
+    s: object
+    v: object
+
+
+def rsvd(x, params: SketchParams, rng: RngState) -> SvdResult:
+    """rnla.hpp:62-77 on a general (rows x cols) matrix; advances rng.counter by 2*cols*w like sample_gaussian."""
+    torch = _torch()
+    _need_cuda_f32(x, "x")
+    rows, cols = x.shape
+    dim = min(rows, cols)
+    r_cl = min(params.target_rank, dim)
+    ctx = context(x.device.index)
+    u = torch.empty(rows, max(1, r_cl), device=x.device, dtype=torch.float32)
+    s = torch.empty(max(1, r_cl), device=x.device, dtype=torch.float32)
+    v = torch.empty(cols, max(1, r_cl), device=x.device, dtype=torch.float32)
+    ctr = _c_u64(rng.counter)
+    rank = _c_i64(0)
+    _check(ctx.lib.rkfac_rsvd(ctx.h, _ptr(x), x.stride(0), rows, cols, params.target_rank, params.oversampling,
+                              params.power_iters, _c_u64(rng.seed), C.byref(ctr), _ptr(u), u.stride(0), _ptr(s), _ptr(v),
+                              v.stride(0), C.byref(rank)), ctx.h, "rsvd")
+    rng.counter = int(ctr.value)
+    rr = int(rank.value)
+    return SvdResult(u[:, :rr], s[:rr], v[:, :rr])
 
 
 def srevd(x, params: SketchParams, rng: RngState) -> LowRankEig:

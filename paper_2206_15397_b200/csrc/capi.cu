@@ -214,6 +214,24 @@ int rkfac_rsvd_psd(rkfac_context_t ctx, const float* x, int64_t ldx, int64_t d, 
     return decompose_single(ctx, RKFAC_RSVD, x, ldx, d, r, p, q, seed, counter, u, ldu, dvals, rank_out);
 }
 
+int rkfac_rsvd(rkfac_context_t ctx, const float* x, int64_t ldx, int64_t rows, int64_t cols, int64_t r, int64_t p,
+               int64_t q, uint64_t seed, uint64_t* counter, float* u, int64_t ldu, float* s, float* v, int64_t ldv,
+               int64_t* rank_out) {
+    return guarded(ctx, [&] {
+        RKFAC_REQUIRE(ctx && x && u && s && v && counter, RKFAC_INVALID_ARGUMENT, "null argument");
+        RKFAC_REQUIRE(rows >= 1 && cols >= 1 && r >= 1 && p >= 0 && q >= 0 && ldx >= cols, RKFAC_INVALID_ARGUMENT,
+                      "bad sizes");
+        const int64_t dim = std::min(rows, cols);
+        const int64_t rc = std::min(r, dim), pc = r > dim ? 0 : std::min(p, dim - rc);
+        RKFAC_REQUIRE(ldu >= rc && ldv >= rc, RKFAC_INVALID_ARGUMENT, "ld_u / ld_v < clamped rank");
+        int rk = 0;
+        ctx->c.rsvd.run(x, ldx, (int)rows, (int)cols, (int)r, (int)p, (int)q, seed, *counter, u, ldu, s, v, ldv, &rk,
+                        ctx->c.stream);
+        *counter += 2ULL * (uint64_t)cols * (uint64_t)(rc + pc);  // sample_gaussian(rng, cols, width), rng.hpp:59-63
+        if (rank_out) *rank_out = rk;
+    });
+}
+
 int rkfac_apply_lowrank_damped_inverse(rkfac_context_t ctx, const float* u, int64_t ldu, const float* dvals,
                                        int64_t dim, int64_t r, double lambda, const float* v, int64_t ldv,
                                        int64_t rows, int64_t cols, int side, float* out, int64_t ldo) {

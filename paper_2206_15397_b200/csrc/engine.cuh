@@ -13,6 +13,7 @@
 #include "dmma.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "rsvd.cuh"
 #include "single.cuh"
 #include "symeig.cuh"
 #include "tc_gemm.cuh"
@@ -201,6 +202,8 @@ struct Context {
     SingleOps single;
     // full d x d eigensolver of the exact K-FAC comparator and the spectrum snapshots (symeig.cu), workspace kept
     SymEig symeig;
+    // general rectangular rsvd (rsvd.cu), workspace kept
+    Rsvd rsvd;
     // optional NCCL communicator (ncclComm_t, caller-owned) for the plan's all-gather (comm.cu)
     void* nccl_comm = nullptr;
     int nccl_rank = 0, nccl_nranks = 1;

@@ -96,8 +96,17 @@ def test_plan_ea_long_k_n512_matches_oracle(port, cuda, mode):
     _ea_case(port, cuda, [rk.LayerSpec(2048, 640)], 512, 1.2, mode, 3, 1)
 
 
+# init, and the bars for the reconstruction / eigenvalues / preconditioned gradient.  Zero init (the parity
+# fixtures): north_star's 1e-4.  Identity init (the reference default, kfactor.hpp:27) is the labelled
+# robustness row of SURVEY 8(d): the eigenvalues just above the identity's unit floor are nearly degenerate, so FP32
+# input rounding alone moves the reconstruction by ~2e-4 and the gradient by ~8e-5 (d = 512) -- the
+# reconstruction and gradient bars are relaxed (gap-aware), the eigenvalue bar is not.
+INIT_BARS = {"zero": (1e-4, 1e-4, 1e-4), "eye": (2e-3, 1e-4, 1e-3)}
+
+
 @pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref (the reference build) not present")
-def test_config3_full_step_as_benched_matches_reference(cuda):
+@pytest.mark.parametrize("init", ["zero", "eye"])
+def test_config3_full_step_as_benched_matches_reference(cuda, init):
     """BASELINE config 3, the bench's workload, through the bench's own code path; the reference's whole step
     (EA -> 32 srevd -> 16 RIGHT/LEFT preconditionings, ref_step_threaded over the unmodified reference headers) on
     the same inputs: the GPU's FP32 factors after the 20 warm-up EA steps, the timed step's samples and gradients."""
@@ -110,6 +119,9 @@ def test_config3_full_step_as_benched_matches_reference(cuda):
     specs = [rk.LayerSpec(a, g) for a, g in layers]
     st = rk.StreamedStep(specs, groups=5, rank=r, oversampling=p, power_iters=q, method=rk.DecompMethod.SREVD,
                          n_samples=[n], device=0)
+    if init == "eye":
+        for x in st.factors:
+            x.copy_(torch.eye(x.shape[0], device=cuda))
     inv_sqrt_n = 1.0 / math.sqrt(n)
 
     def fill_samples(k):  # bench.run_ours.fill_samples
@@ -151,9 +163,10 @@ def test_config3_full_step_as_benched_matches_reference(cuda):
         worst["eig"] = max(worst["eig"], eig_err(np64(lr.d), d0))
     for l in range(len(layers)):
         worst["grad"] = max(worst["grad"], rel_fro(np64(st.outs[l]), outs[l]))
-    print("config-3 step vs reference, worst over factors/layers:", worst)
+    print(f"config-3 step ({init} init) vs reference, worst over factors/layers:", worst)
     assert worst["ea"] < EA_TOL_PER_K * n
-    assert worst["recon"] < TOL and worst["eig"] < TOL and worst["grad"] < TOL, worst
+    b_rec, b_eig, b_grad = INIT_BARS[init]
+    assert worst["recon"] < b_rec and worst["eig"] < b_eig and worst["grad"] < b_grad, worst
 
 
 GOLD5 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config5_golden.npz")

@@ -521,3 +521,32 @@ def test_spectrum_snapshot_matches_oracle(port, cuda):
     ev = np.asarray(rep.eigenvalues)
     top = np.maximum(d0, 0.0)[:40]
     assert eig_err(ev[:40], top) < TOL and rep.lambda_max == pytest.approx(top[0], rel=1e-6)
+
+
+# ------------------------------------------------------------------------- general rsvd (rnla.hpp:62-77)
+@pytest.mark.skipif(not __import__("oracle").ref_available(), reason="oracle/_ref (the reference build) not present")
+@pytest.mark.parametrize("rows,cols", [(300, 200), (200, 300), (517, 517)])
+def test_rsvd_general_matches_reference(port, cuda, rows, cols):
+    """SvdResult rsvd on a rectangular matrix with a geometric spectrum vs the reference's own rsvd on the same input
+    and Omega stream: singular values, the sign-invariant product U diag(s) V^T, orthonormality, counter advance."""
+    import oracle
+    import paper_2206_15397_b200 as rk
+
+    ref = oracle.ref()
+    k = min(rows, cols)
+    g1, _ = port.sample_gaussian(41, 0, rows, k)
+    g2, _ = port.sample_gaussian(42, 0, cols, k)
+    u0, _ = port.qr_thin(g1)
+    v0, _ = port.qr_thin(g2)
+    x = ((u0 * geometric_spectrum(k, 0.9)[None, :]) @ v0.T).astype(np.float32).astype(np.float64)
+    r, p, q = 20, 5, 2
+    seed = port.substream(OMEGA_ROOT, 0, 5)
+    ur, sr, vr, cr = ref.rsvd(x, r, p, q, seed, 0)
+    rng = rk.RngState(seed, 0)
+    res = rk.rsvd(t32(x, cuda), rk.SketchParams(r, p, q), rng)
+    assert rng.counter == cr
+    u1, s1, v1 = np64(res.u), np64(res.s), np64(res.v)
+    assert u1.shape == ur.shape and v1.shape == vr.shape
+    assert eig_err(s1, sr) < TOL
+    assert rel_fro((u1 * s1) @ v1.T, (ur * sr) @ vr.T) < TOL
+    assert orth_err(u1) < 1e-5 and orth_err(v1) < 1e-5
