@@ -762,12 +762,14 @@ class StreamedStep:
             sub.prepare(lam, rho, scale)
 
     def step_host(self, rng_root: int, step: int, lam: float, h_samples, h_grads, h_outs, rho: float = 0.95,
-                  scale: float = 1.0):
+                  scale: float = 1.0, timeline: Optional[list] = None):
         """The step with its inputs and outputs in (pinned) host memory, in the original factor / layer order.
 
         Per group, on the group's stream: H2D of its samples -> EA -> rand-EVD; meanwhile a copy stream brings its
         gradients (needed only by the preconditioning); then precondition -> D2H of its results.  One group's copies
         overlap the other groups' kernels, and every gradient upload overlaps its own group's decomposition.
+        ``timeline`` (a list) receives, per group, timing events (samples in, decomposed, preconditioned, results out)
+        and the fork event first, for tools/e2e_timeline.py.
         """
         if lam <= 0.0:
             raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
@@ -775,8 +777,18 @@ class StreamedStep:
         if not hasattr(self, "_copy_streams"):
             self._copy_streams = [torch.cuda.Stream(device=self.device) for _ in self.subs]
         main = torch.cuda.current_stream(self.device)
-        fork = torch.cuda.Event()
+        timed = timeline is not None
+        fork = torch.cuda.Event(enable_timing=timed)
         fork.record(main)
+        if timed:
+            timeline.append(("fork", fork))
+
+        def mark(st, name, g):
+            if timed:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                timeline.append((f"group{g}:{name}", e))
+
         joins = []
         for g in self._issue_order:  # the critical group's uploads first
             sub, st, cp, part = self.subs[g], self.streams[g], self._copy_streams[g], self.parts[g]
@@ -788,6 +800,7 @@ class StreamedStep:
                             sub.samples[2 * i + w].copy_(h_samples[2 * l + w], non_blocking=True)
                 got_samples = torch.cuda.Event()
                 got_samples.record(st)
+                mark(st, "samples_in", g)
             cp.wait_event(got_samples)  # the gradients follow the samples on the copy engine
             with torch.cuda.stream(cp):
                 for i, l in enumerate(part):
@@ -798,10 +811,13 @@ class StreamedStep:
                 if sub.samples:
                     sub.ea_update(rho, scale)
                 sub.decompose(rng_root, step)
+                mark(st, "decomposed", g)
                 st.wait_event(got_grads)
                 sub.precondition(lam)
+                mark(st, "preconditioned", g)
                 for i, l in enumerate(part):
                     h_outs[l].copy_(sub.outs[i], non_blocking=True)
+                mark(st, "results_out", g)
                 ev = torch.cuda.Event()
                 ev.record(st)
                 joins.append(ev)

@@ -88,8 +88,15 @@ __global__ void copy_kernel(const CopyDesc* __restrict__ descs) {
     for (int r = blockIdx.x * wpb + warp; r < cd.rows; r += gridDim.x * wpb) {
         const float* s = cd.src + (long long)r * cd.lds;
         float* d = cd.dst + (long long)r * cd.ldd;
-        for (int c = lane; c < c4; c += 32)
-            reinterpret_cast<float4*>(d)[c] = reinterpret_cast<const float4*>(s)[c];
+        for (int c0 = lane; c0 < c4; c0 += 4 * 32) {  // four 16-byte loads in flight per lane
+            float4 xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + 32 * u < c4) reinterpret_cast<float4*>(d)[c0 + 32 * u] = xs[u];
+        }
         for (int c = 4 * c4 + lane; c < cd.cols; c += 32) d[c] = s[c];
     }
 }

@@ -840,13 +840,22 @@ __global__ void split_kernel(const SplitDesc* __restrict__ descs) {
         const float* s = sd.src + (long long)r * sd.lds;
         float* h = sd.hi ? sd.hi + (long long)r * sd.ldd : nullptr;
         float* l = sd.lo ? sd.lo + (long long)r * sd.ldd : nullptr;
-        for (int c = lane; c < c4; c += 32) {
-            const float4 x = reinterpret_cast<const float4*>(s)[c];
-            if (h) reinterpret_cast<float4*>(h)[c] = x;
-            if (l)
-                reinterpret_cast<float4*>(l)[c] =
-                    make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
-                                x.w - tf32_trunc(x.w));
+        for (int c0 = lane; c0 < c4; c0 += 4 * 32) {  // four 16-byte loads in flight per lane
+            float4 xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + 32 * u;
+                if (c >= c4) break;
+                const float4 x = xs[u];
+                if (h) reinterpret_cast<float4*>(h)[c] = x;
+                if (l)
+                    reinterpret_cast<float4*>(l)[c] =
+                        make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                    x.w - tf32_trunc(x.w));
+            }
         }
         for (int c = 4 * c4 + lane; c < sd.cols; c += 32) {
             const float x = s[c];
