@@ -653,6 +653,35 @@ class StepGraph:
         self.graph.replay()
 
 
+class HostStepGraph:
+    """``StreamedStep.step_host`` -- the step from pinned host inputs to pinned host outputs, copies included --
+    captured once as one CUDA graph and replayed: the ~100 host-side enqueues of a step (copies and ~70 launches per
+    group) leave the critical path, so every group's samples land and its chain starts at once instead of behind the
+    previous group's enqueue.  Replays read the current contents of the pinned host buffers given at capture (the
+    staging buffers a training loop refills each step) and write the host outputs; bitwise ``step_host``."""
+
+    def __init__(self, step_obj, rng_root: int, step: int, lam: float, h_samples, h_grads, h_outs, rho: float = 0.95,
+                 scale: float = 1.0):
+        torch = _torch()
+        self.step_obj = step_obj
+        step_obj.prepare(lam, rho, scale)
+        dev = step_obj.device
+        step_obj.step_host(rng_root, step, lam, h_samples, h_grads, h_outs, rho, scale)  # streams/events created
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        n0 = step_obj.ctx.launches()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                step_obj.step_host(rng_root, step, lam, h_samples, h_grads, h_outs, rho, scale)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        self.launches = step_obj.ctx.launches() - n0
+
+    def replay(self):
+        self.graph.replay()
+
+
 class StreamedStep:
     """The batched step split into ``groups`` independent layer groups, each a :class:`BatchedStep` (its own plan)
     run on its own CUDA stream and joined back into the caller's stream.
@@ -789,30 +818,41 @@ class StreamedStep:
                 e.record(st)
                 timeline.append((f"group{g}:{name}", e))
 
-        joins = []
+        # 1. every group's samples first (the host-to-device engine serves copies in submission order: a group's
+        #    gradients, needed only at the end of its chain, must not delay the next group's samples), each group's
+        #    EA + rand-EVD enqueued right behind its own samples
+        last_samples = None
         for g in self._issue_order:  # the critical group's uploads first
-            sub, st, cp, part = self.subs[g], self.streams[g], self._copy_streams[g], self.parts[g]
+            sub, st, part = self.subs[g], self.streams[g], self.parts[g]
             st.wait_event(fork)
             with torch.cuda.stream(st):
                 for i, l in enumerate(part):
                     for w in (0, 1):
                         if sub.samples:
                             sub.samples[2 * i + w].copy_(h_samples[2 * l + w], non_blocking=True)
-                got_samples = torch.cuda.Event()
-                got_samples.record(st)
+                last_samples = torch.cuda.Event()
+                last_samples.record(st)
                 mark(st, "samples_in", g)
-            cp.wait_event(got_samples)  # the gradients follow the samples on the copy engine
-            with torch.cuda.stream(cp):
-                for i, l in enumerate(part):
-                    sub.grads[i].copy_(h_grads[l], non_blocking=True)
-                got_grads = torch.cuda.Event()
-                got_grads.record(cp)
-            with torch.cuda.stream(st):
                 if sub.samples:
                     sub.ea_update(rho, scale)
                 sub.decompose(rng_root, step)
                 mark(st, "decomposed", g)
-                st.wait_event(got_grads)
+        # 2. the gradients, behind all the samples on the copy engine
+        got_grads = {}
+        for g in self._issue_order:
+            sub, cp, part = self.subs[g], self._copy_streams[g], self.parts[g]
+            cp.wait_event(last_samples)
+            with torch.cuda.stream(cp):
+                for i, l in enumerate(part):
+                    sub.grads[i].copy_(h_grads[l], non_blocking=True)
+                got_grads[g] = torch.cuda.Event()
+                got_grads[g].record(cp)
+        # 3. per group: precondition -> results to the host
+        joins = []
+        for g in self._issue_order:
+            sub, st, part = self.subs[g], self.streams[g], self.parts[g]
+            with torch.cuda.stream(st):
+                st.wait_event(got_grads[g])
                 sub.precondition(lam)
                 mark(st, "preconditioned", g)
                 for i, l in enumerate(part):

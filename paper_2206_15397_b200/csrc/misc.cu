@@ -78,26 +78,32 @@ __global__ void bracket_kernel(const BracketDesc* __restrict__ descs, double lam
     }
 }
 
-// One descriptor per blockIdx.y, one row per warp, float4 accesses when both rows are 16-byte aligned.
+// One descriptor per blockIdx.y; work items are (row, 2 KB chunk) pairs spread over the warps of the descriptor's
+// blocks, four 16-byte loads in flight per lane (a few long rows -- a 512 x 4609 gradient -- still fill the GPU).
 __global__ void copy_kernel(const CopyDesc* __restrict__ descs) {
     const CopyDesc cd = descs[blockIdx.y];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const bool vec = ((reinterpret_cast<uintptr_t>(cd.src) | reinterpret_cast<uintptr_t>(cd.dst) |
                        (uintptr_t)(cd.lds * 4) | (uintptr_t)(cd.ldd * 4)) & 15) == 0;
     const int c4 = vec ? cd.cols / 4 : 0;
-    for (int r = blockIdx.x * wpb + warp; r < cd.rows; r += gridDim.x * wpb) {
+    const int chunks = (c4 + 127) / 128 + 1;  // the last chunk also takes the scalar tail
+    const long long items = (long long)cd.rows * chunks;
+    for (long long it = blockIdx.x * wpb + warp; it < items; it += (long long)gridDim.x * wpb) {
+        const int r = (int)(it / chunks), ch = (int)(it - (long long)r * chunks);
         const float* s = cd.src + (long long)r * cd.lds;
         float* d = cd.dst + (long long)r * cd.ldd;
-        for (int c0 = lane; c0 < c4; c0 += 4 * 32) {  // four 16-byte loads in flight per lane
-            float4 xs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c0 + 32 * u < c4) reinterpret_cast<float4*>(d)[c0 + 32 * u] = xs[u];
+        if (ch + 1 == chunks) {
+            for (int c = 4 * c4 + lane; c < cd.cols; c += 32) d[c] = s[c];
+            continue;
         }
-        for (int c = 4 * c4 + lane; c < cd.cols; c += 32) d[c] = s[c];
+        const int c0 = ch * 128 + lane;
+        float4 xs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (c0 + 32 * u < c4) reinterpret_cast<float4*>(d)[c0 + 32 * u] = xs[u];
     }
 }
 

@@ -829,38 +829,44 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const TcProb* __restrict
     }
 }
 
-// One descriptor per blockIdx.y, one row per warp, float4 accesses when every row involved is 16-byte aligned.
+// One descriptor per blockIdx.y; work items are (row, 2 KB chunk) pairs spread over the warps of the descriptor's
+// blocks, float4 accesses (four in flight per lane) when every row involved is 16-byte aligned.
 __global__ void split_kernel(const SplitDesc* __restrict__ descs) {
     const SplitDesc sd = descs[blockIdx.y];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const bool vec = ((reinterpret_cast<uintptr_t>(sd.src) | reinterpret_cast<uintptr_t>(sd.hi) |
                        reinterpret_cast<uintptr_t>(sd.lo) | (uintptr_t)(sd.lds * 4) | (uintptr_t)(sd.ldd * 4)) & 15) == 0;
     const int c4 = vec ? sd.cols / 4 : 0;
-    for (int r = blockIdx.x * wpb + warp; r < sd.rows; r += gridDim.x * wpb) {
+    const int chunks = (c4 + 127) / 128 + 1;  // the last chunk also takes the scalar tail
+    const long long items = (long long)sd.rows * chunks;
+    for (long long it = blockIdx.x * wpb + warp; it < items; it += (long long)gridDim.x * wpb) {
+        const int r = (int)(it / chunks), ch = (int)(it - (long long)r * chunks);
         const float* s = sd.src + (long long)r * sd.lds;
         float* h = sd.hi ? sd.hi + (long long)r * sd.ldd : nullptr;
         float* l = sd.lo ? sd.lo + (long long)r * sd.ldd : nullptr;
-        for (int c0 = lane; c0 < c4; c0 += 4 * 32) {  // four 16-byte loads in flight per lane
-            float4 xs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int c = c0 + 32 * u;
-                if (c >= c4) break;
-                const float4 x = xs[u];
-                if (h) reinterpret_cast<float4*>(h)[c] = x;
-                if (l)
-                    reinterpret_cast<float4*>(l)[c] =
-                        make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
-                                    x.w - tf32_trunc(x.w));
+        if (ch + 1 == chunks) {
+            for (int c = 4 * c4 + lane; c < sd.cols; c += 32) {
+                const float x = s[c];
+                if (h) h[c] = x;
+                if (l) l[c] = x - tf32_trunc(x);
             }
+            continue;
         }
-        for (int c = 4 * c4 + lane; c < sd.cols; c += 32) {
-            const float x = s[c];
-            if (h) h[c] = x;
-            if (l) l[c] = x - tf32_trunc(x);
+        const int c0 = ch * 128 + lane;
+        float4 xs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (c0 + 32 * u < c4) xs[u] = reinterpret_cast<const float4*>(s)[c0 + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 32 * u;
+            if (c >= c4) break;
+            const float4 x = xs[u];
+            if (h) reinterpret_cast<float4*>(h)[c] = x;
+            if (l)
+                reinterpret_cast<float4*>(l)[c] =
+                    make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                x.w - tf32_trunc(x.w));
         }
     }
 }
