@@ -9,6 +9,10 @@
 //   LowRankEig rsvd_psd(...same...)                        rkfac::gpu::rsvd_psd         (rnla.hpp:81-85)
 //   DenseMatrix apply_lowrank_damped_inverse(const LowRankEig&, double, const DenseMatrix&, ApplySide)
 //                                                          rkfac::gpu::apply_lowrank_damped_inverse (kfactor.hpp:134-161)
+//   SvdResult rsvd(const DenseMatrix&, const SketchParams&, RngState&)   rkfac::gpu::rsvd  (rnla.hpp:62-77)
+//   SymEigResult sym_eig(const DenseMatrix&)                rkfac::gpu::sym_eig          (eig.hpp:210-237)
+//   DenseMatrix apply_eig_damped_inverse(const SymEigResult&, double, const DenseMatrix&, ApplySide)
+//                                                          rkfac::gpu::apply_eig_damped_inverse (kfactor.hpp:182-185)
 //
 // Value semantics as in the reference: inputs by const&, outputs by value, EAKFactor mutated in place, RngState&
 // advanced by 2*d*w exactly like sample_gaussian (rng.hpp:59-63).  FP64 host data is converted to FP32 for the
@@ -139,6 +143,65 @@ inline DenseMatrix apply_lowrank_damped_inverse(const LowRankEig& lr, double lam
     detail::check(rkfac_synchronize(detail::context()), "apply_lowrank_damped_inverse");
     DenseMatrix out(v.rows(), v.cols());
     dout.download(out.data(), out.size());
+    return out;
+}
+
+// eig.hpp:210-237: full symmetric eigendecomposition (FP64 on the GPU: Householder + divide and conquer), eigenvectors
+// as the columns of p, eigenvalues descending; asymmetry -> DimensionMismatch, a non-converging leaf -> NoConvergence.
+inline SymEigResult sym_eig(const DenseMatrix& s) {
+    if (s.rows() != s.cols()) throw DimensionMismatch("sym_eig: matrix must be square");
+    const std::size_t n = s.rows();
+    detail::DevMat ds(s), dp(n, n);
+    double* d64 = nullptr;
+    if (cudaMalloc(&d64, sizeof(double) * std::max<std::size_t>(n, 1)) != cudaSuccess) throw std::bad_alloc();
+    const int st = rkfac_sym_eig(detail::context(), ds.p, (int64_t)n, (int64_t)n, dp.p, (int64_t)n, nullptr, d64);
+    SymEigResult out;
+    out.d.resize(n);
+    if (st == RKFAC_OK) cudaMemcpy(out.d.data(), d64, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaFree(d64);
+    detail::check(st, "sym_eig");
+    out.p = DenseMatrix(n, n);
+    dp.download(out.p.data(), out.p.size());
+    return out;
+}
+
+// kfactor.hpp:165-186: the exact damped inverse through the low-rank kernels (Eq. 11 with a complete orthonormal
+// basis is exactly (U D U^T + lambda I)^{-1}).
+inline DenseMatrix apply_eig_damped_inverse(const SymEigResult& eig, double lambda, const DenseMatrix& v,
+                                            ApplySide side) {
+    if (lambda <= 0.0) throw DampingNonpositive("apply_eig_damped_inverse: lambda must be > 0");
+    LowRankEig lr;
+    lr.u = eig.p;
+    lr.d = eig.d;
+    lr.method = DecompMethod::SREVD;
+    return rkfac::gpu::apply_lowrank_damped_inverse(lr, lambda, v, side);
+}
+
+// rnla.hpp:62-77 on a general rows x cols matrix.
+inline SvdResult rsvd(const DenseMatrix& x, const SketchParams& p, RngState& rng) {
+    const std::size_t rows = x.rows(), cols = x.cols();
+    const std::size_t rmax = std::max<std::size_t>(1, std::min({p.target_rank, rows, cols}));
+    detail::DevMat dx(x), du(rows, rmax), ds(rmax, 1), dv(cols, rmax);
+    uint64_t counter = rng.counter;
+    int64_t rank = 0;
+    detail::check(rkfac_rsvd(detail::context(), dx.p, (int64_t)cols, (int64_t)rows, (int64_t)cols,
+                             (int64_t)p.target_rank, (int64_t)p.oversampling, (int64_t)p.power_iters, rng.seed,
+                             &counter, du.p, (int64_t)rmax, ds.p, dv.p, (int64_t)rmax, &rank),
+                  "rsvd");
+    rng.counter = counter;
+    const std::size_t r = (std::size_t)rank;
+    std::vector<double> u(rows * rmax), s(rmax), v(cols * rmax);
+    du.download(u.data(), u.size());
+    ds.download(s.data(), s.size());
+    dv.download(v.data(), v.size());
+    SvdResult out;
+    out.u = DenseMatrix(rows, r);
+    out.v = DenseMatrix(cols, r);
+    for (std::size_t i = 0; i < rows; ++i)
+        for (std::size_t j = 0; j < r; ++j) out.u(i, j) = u[i * rmax + j];
+    for (std::size_t i = 0; i < cols; ++i)
+        for (std::size_t j = 0; j < r; ++j) out.v(i, j) = v[i * rmax + j];
+    out.s.assign(s.begin(), s.begin() + r);
     return out;
 }
 

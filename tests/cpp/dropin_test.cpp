@@ -55,6 +55,36 @@ int main() {
         std::printf(", \"%s\": {\"recon\": %.3e, \"eig\": %.3e, \"precond\": %.3e, \"counter_match\": %d}",
                     meth == 0 ? "srevd" : "rsvd_psd", e_rec, e_eig, e_s, int(r0.counter == r1.counter));
     }
+    // exact K-FAC (eig.hpp:210-237 + kfactor.hpp:182-185) and the general rsvd (rnla.hpp:62-77)
+    {
+        const SymEigResult ea = sym_eig(f_cpu.mbar), eb = gpu::sym_eig(f_cpu.mbar);
+        double e_eig = 0.0;
+        for (std::size_t i = 0; i < 40; ++i) e_eig = std::max(e_eig, std::abs(ea.d[i] - eb.d[i]) / std::abs(ea.d[i]));
+        const DenseMatrix sa = apply_eig_damped_inverse(ea, 0.1, j, ApplySide::LEFT);
+        const DenseMatrix sb = gpu::apply_eig_damped_inverse(eb, 0.1, j, ApplySide::LEFT);
+        const double e_s = rel(sb, sa);
+        const bool ok = e_eig < 1e-6 && e_s < 1e-4;
+        fails += ok ? 0 : 1;
+        std::printf(", \"sym_eig\": {\"eig_top40\": %.3e, \"precond\": %.3e}", e_eig, e_s);
+        RngState g_x = RngState(5).substream(0, 0);
+        const DenseMatrix xr = sample_gaussian(g_x, 150, 100);
+        DenseMatrix xs(150, 100);  // geometric column decay so the sketch is well posed
+        for (std::size_t i = 0; i < 150; ++i)
+            for (std::size_t c = 0; c < 100; ++c) xs(i, c) = xr(i, c) * std::pow(0.9, double(c));
+        RngState r0 = RngState(7).substream(0, 3), r1 = r0;
+        const SvdResult a = rsvd(xs, SketchParams{12, 4, 2}, r0), b = gpu::rsvd(xs, SketchParams{12, 4, 2}, r1);
+        DenseMatrix pa(150, 100), pb(150, 100);
+        for (std::size_t i = 0; i < 150; ++i)
+            for (std::size_t c = 0; c < 100; ++c)
+                for (std::size_t k = 0; k < a.s.size(); ++k) {
+                    pa(i, c) += a.u(i, k) * a.s[k] * a.v(c, k);
+                    pb(i, c) += b.u(i, k) * b.s[k] * b.v(c, k);
+                }
+        const double e_p = rel(pb, pa);
+        const bool ok2 = r0.counter == r1.counter && e_p < 1e-4 && b.s.size() == a.s.size();
+        fails += ok2 ? 0 : 1;
+        std::printf(", \"rsvd\": {\"usv\": %.3e, \"counter_match\": %d}", e_p, int(r0.counter == r1.counter));
+    }
     // error behaviour mirrors the reference exceptions
     bool threw = false;
     try {

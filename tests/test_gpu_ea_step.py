@@ -110,11 +110,12 @@ GAP_MIN = 1e-3
 
 
 @pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref (the reference build) not present")
-@pytest.mark.parametrize("init", ["zero", "eye"])
-def test_config3_full_step_as_benched_matches_reference(cuda, init):
+@pytest.mark.parametrize("init,method", [("zero", "srevd"), ("eye", "srevd"), ("zero", "rsvd_psd")])
+def test_config3_full_step_as_benched_matches_reference(cuda, init, method):
     """BASELINE config 3, the bench's workload, through the bench's own code path; the reference's whole step
-    (EA -> 32 srevd -> 16 RIGHT/LEFT preconditionings, ref_step_threaded over the unmodified reference headers) on
-    the same inputs: the GPU's FP32 factors after the 20 warm-up EA steps, the timed step's samples and gradients."""
+    (EA -> 32 srevd (or rsvd_psd: RS-KFAC, optimizer.hpp:182-192) -> 16 RIGHT/LEFT preconditionings,
+    ref_step_threaded over the unmodified reference headers) on the same inputs: the GPU's FP32 factors after the 20
+    warm-up EA steps, the timed step's samples and gradients."""
     import torch
     import paper_2206_15397_b200 as rk
 
@@ -122,7 +123,8 @@ def test_config3_full_step_as_benched_matches_reference(cuda, init):
 
     layers, n, e, r, p, q, lam, warm = bench.WORKLOADS["vgg16"]
     specs = [rk.LayerSpec(a, g) for a, g in layers]
-    st = rk.StreamedStep(specs, groups=5, rank=r, oversampling=p, power_iters=q, method=rk.DecompMethod.SREVD,
+    meth = rk.DecompMethod.SREVD if method == "srevd" else rk.DecompMethod.RSVD
+    st = rk.StreamedStep(specs, groups=5, rank=r, oversampling=p, power_iters=q, method=meth,
                          n_samples=[n], device=0)
     if init == "eye":
         for x in st.factors:
@@ -155,9 +157,9 @@ def test_config3_full_step_as_benched_matches_reference(cuda, init):
     threads = os.cpu_count() or 1
     us = [np.zeros((d, min(r, d))) for d in st.dims]
     dvs = [np.zeros(min(r, d)) for d in st.dims]
-    ph = ref.step_threaded("srevd", threads, dims_a, dims_g, factors, ms, [n] * len(ms), 0.95, r, p, q, OMEGA_ROOT,
+    ph = ref.step_threaded(method, threads, dims_a, dims_g, factors, ms, [n] * len(ms), 0.95, r, p, q, OMEGA_ROOT,
                            0, lam, grads, outs, us, dvs)
-    print(f"reference step on {threads} threads: EA {ph[0]:.1f}s, srevd {ph[1]:.1f}s, apply {ph[2]:.1f}s")
+    print(f"reference step on {threads} threads: EA {ph[0]:.1f}s, {method} {ph[1]:.1f}s, apply {ph[2]:.1f}s")
     decs = [(us[f], dvs[f], None) for f in range(len(us))]  # `factors` now hold the reference's EA result
     worst = {"recon": 0.0, "eig": 0.0, "grad": 0.0, "ea": 0.0}
     gaps, rec = [], []
@@ -175,7 +177,7 @@ def test_config3_full_step_as_benched_matches_reference(cuda, init):
     worst["recon"] = max([e for e, g in zip(rec, gaps) if g > gate], default=0.0)
     grad_err = [rel_fro(np64(st.outs[l]), outs[l]) for l in range(len(layers))]
     worst["grad"] = max([e for l, e in enumerate(grad_err) if min(gaps[2 * l], gaps[2 * l + 1]) > gate], default=0.0)
-    print(f"config-3 step ({init} init) vs reference, worst over the gated factors/layers:", worst)
+    print(f"config-3 step ({init} init, {method}) vs reference, worst over the gated factors/layers:", worst)
     print("  per factor (relative gap at r, reconstruction):",
           [(st.dims[f], f"{gaps[f]:.1e}", f"{rec[f]:.1e}") for f in range(len(factors))])
     print("  per layer gradient:", [f"{e:.1e}" for e in grad_err])
