@@ -86,14 +86,22 @@ __global__ void copy_kernel(const CopyDesc* __restrict__ descs) {
     const bool vec = ((reinterpret_cast<uintptr_t>(cd.src) | reinterpret_cast<uintptr_t>(cd.dst) |
                        (uintptr_t)(cd.lds * 4) | (uintptr_t)(cd.ldd * 4)) & 15) == 0;
     const int c4 = vec ? cd.cols / 4 : 0;
-    const int chunks = (c4 + 127) / 128 + 1;  // the last chunk also takes the scalar tail
+    // chunks: 2 KB float4 chunks, then 1 KB scalar chunks for the rest (a whole unaligned row), 8 loads in flight
+    const int nvec = (c4 + 127) / 128, nsc = (cd.cols - 4 * c4 + 255) / 256, chunks = nvec + nsc;
     const long long items = (long long)cd.rows * chunks;
     for (long long it = blockIdx.x * wpb + warp; it < items; it += (long long)gridDim.x * wpb) {
         const int r = (int)(it / chunks), ch = (int)(it - (long long)r * chunks);
         const float* s = cd.src + (long long)r * cd.lds;
         float* d = cd.dst + (long long)r * cd.ldd;
-        if (ch + 1 == chunks) {
-            for (int c = 4 * c4 + lane; c < cd.cols; c += 32) d[c] = s[c];
+        if (ch >= nvec) {
+            const int cb = 4 * c4 + (ch - nvec) * 256 + lane;
+            float xs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cb + 32 * u < cd.cols) xs[u] = s[cb + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cb + 32 * u < cd.cols) d[cb + 32 * u] = xs[u];
             continue;
         }
         const int c0 = ch * 128 + lane;

@@ -837,18 +837,26 @@ __global__ void split_kernel(const SplitDesc* __restrict__ descs) {
     const bool vec = ((reinterpret_cast<uintptr_t>(sd.src) | reinterpret_cast<uintptr_t>(sd.hi) |
                        reinterpret_cast<uintptr_t>(sd.lo) | (uintptr_t)(sd.lds * 4) | (uintptr_t)(sd.ldd * 4)) & 15) == 0;
     const int c4 = vec ? sd.cols / 4 : 0;
-    const int chunks = (c4 + 127) / 128 + 1;  // the last chunk also takes the scalar tail
+    // chunks: 2 KB float4 chunks, then 1 KB scalar chunks for the rest (a whole unaligned row), 8 loads in flight
+    const int nvec = (c4 + 127) / 128, nsc = (sd.cols - 4 * c4 + 255) / 256, chunks = nvec + nsc;
     const long long items = (long long)sd.rows * chunks;
     for (long long it = blockIdx.x * wpb + warp; it < items; it += (long long)gridDim.x * wpb) {
         const int r = (int)(it / chunks), ch = (int)(it - (long long)r * chunks);
         const float* s = sd.src + (long long)r * sd.lds;
         float* h = sd.hi ? sd.hi + (long long)r * sd.ldd : nullptr;
         float* l = sd.lo ? sd.lo + (long long)r * sd.ldd : nullptr;
-        if (ch + 1 == chunks) {
-            for (int c = 4 * c4 + lane; c < sd.cols; c += 32) {
-                const float x = s[c];
-                if (h) h[c] = x;
-                if (l) l[c] = x - tf32_trunc(x);
+        if (ch >= nvec) {
+            const int cb = 4 * c4 + (ch - nvec) * 256 + lane;
+            float xs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cb + 32 * u < sd.cols) xs[u] = s[cb + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int c = cb + 32 * u;
+                if (c >= sd.cols) break;
+                if (h) h[c] = xs[u];
+                if (l) l[c] = xs[u] - tf32_trunc(xs[u]);
             }
             continue;
         }
@@ -1007,7 +1015,9 @@ void TcGemm::finalize() {
         }
     }
     // Paired tiles halve the B traffic but also the number of schedulable units: keep them only when the paired
-    // units still fill every SM (pairing never changes the arithmetic, so this may depend on the batch).
+    // units still fill every SM (pairing never changes the arithmetic, so this may depend on the batch).  Splitting
+    // the pairs longer than a CTA's average load as well was measured: VGG16's X*Q 3.29 -> 4.01 ms (the B re-reads
+    // cost more than the better balance gains).
     {
         long long units = 0, paired_units = (long long)tiles_.size();
         for (const auto& t : tiles_) units += t.pair ? 2 : 1;
