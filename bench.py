@@ -517,6 +517,25 @@ def run_ours(args, wl):
         torch.cuda.cudart().cudaProfilerStop()
         return
 
+    if args.trace:  # the concurrent kernel timeline of one step (CUPTI through torch.profiler) -> tools/timeline.py
+        from torch.profiler import ProfilerActivity, profile
+
+        reset()
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            one_step()
+            torch.cuda.synchronize()
+        rows = [{"name": e.name, "ts": e.time_range.start, "dur": e.time_range.end - e.time_range.start,
+                 "stream": getattr(e, "stream", None) if hasattr(e, "stream") else None}
+                for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+        try:  # the chrome trace carries stream / grid per kernel
+            prof.export_chrome_trace(args.trace)
+        except Exception as ex:  # noqa: BLE001
+            print("chrome trace failed:", ex, file=sys.stderr)
+            with open(args.trace, "w") as fh:
+                json.dump(rows, fh)
+        return
+
     # ---- timed region: K steps (factor restore is outside the events) ----
     stream = torch.cuda.current_stream(dev)
     launches0 = ctx.launches()
@@ -683,6 +702,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=5, help="layer groups on concurrent streams (StreamedStep; 5 gave the best e2e)")
     ap.add_argument("--profile-step", action="store_true", help="run one step under cudaProfilerStart/Stop and exit")
+    ap.add_argument("--trace", default="", help="write the kernel timeline of one step (chrome trace) and exit")
     ap.add_argument("--emulate-world", type=int, default=0, help="run one shard of an N-GPU job alone (projection)")
     ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--e2e-graph", action=argparse.BooleanOptionalAction, default=True,

@@ -73,6 +73,17 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
     RKFAC_REQUIRE(method == RKFAC_SREVD || method == RKFAC_RSVD, RKFAC_INVALID_ARGUMENT, "unknown method");
     f_.resize(n);
     if (const char* nf = std::getenv("RKFAC_FP64_ORTHS")) n_fp64_orth_ = std::atoi(nf);
+    if (const char* ov = std::getenv("RKFAC_OVERLAP_ORTH")) overlap_orth_ = std::atoi(ov) != 0;
+    if (const char* et = std::getenv("RKFAC_EXPLICIT_TAIL")) explicit_tail_ = std::max(0, std::atoi(et));
+    {
+        // side stream of the overlapped power iteration (Gram + Cholesky-inverse next to the product): the latency-
+        // bound chain gets the highest priority so its small grids take SMs as soon as they drain
+        int lo_pri = 0, hi_pri = 0;
+        RKFAC_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        RKFAC_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi_pri));
+        RKFAC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        RKFAC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
     Carver c;
     struct Offs {
         size_t S[2][4], Xc, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
@@ -165,6 +176,9 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
 
 Plan::~Plan() {
     for (auto& e : pool_) cudaEventDestroy(e);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (side_) cudaStreamDestroy(side_);
 }
 
 double Plan::xq_flops() const {
@@ -317,6 +331,8 @@ void Plan::build_decomp_stages() {
         xq_[dir] = new_tc();
         xqf_[dir] = new_tc();
         xq_t_[dir] = new_tc();
+        xq_tl_[dir] = new_tc();
+        xz_[dir] = new_tc();
         gram_[dir] = new_tc();
         tri_[dir] = new_tc();
         tri_t_[dir] = new_tc();
@@ -350,6 +366,16 @@ void Plan::build_decomp_stages() {
                 pt.out1 = TcOut{};
                 pt.lo0 = TcOut{};  // the FP64 Gram and Y L^-T read Y^T itself (FP64 DMMA), not its TF32 lo plane
                 xq_t_[dir]->add(pt);
+                // the overlapped power iteration (decompose): Y1 = X Q0 feeds the Gram and the next product (Y^T and
+                // its lo plane only); Z = X Y is read by Z L^-T as a row-major operand only
+                TcProblemDesc ptl = p;
+                ptl.out1 = TcOut{};
+                xq_tl_[dir]->add(ptl);
+                TcProblemDesc pz = p;
+                pz.out0 = out_r(Y.R, F.wp);
+                pz.out1 = TcOut{};
+                pz.lo0 = TcOut{};
+                xz_[dir]->add(pz);
                 p.slice_k = kSliceKFinal;
                 if (method_ == RKFAC_SREVD) p.out1 = TcOut{};
                 xqf_[dir]->add(p);
@@ -409,7 +435,8 @@ void Plan::build_decomp_stages() {
             return !(e && e[0] == '0');
         }();
         gram_[dir]->set_defer_reduce(fuse_gram);  // the Cholesky-inverse sums the Gram's K slices while loading it
-        xq_[dir]->finalize(); xqf_[dir]->finalize(); xq_t_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); tri_t_[dir]->finalize(); core_[dir]->finalize();
+        xq_[dir]->finalize(); xqf_[dir]->finalize(); xq_t_[dir]->finalize(); xq_tl_[dir]->finalize();
+        xz_[dir]->finalize(); gram_[dir]->finalize(); tri_[dir]->finalize(); tri_t_[dir]->finalize(); core_[dir]->finalize();
         gram64_[dir]->finalize(); tri64_[dir]->finalize(); lift_[dir]->finalize();
     }
     std::vector<CopyDesc> cp;
@@ -676,7 +703,17 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     };
     // Every product is orthonormalised, as in the reference: skipping alternate orthonormalisations (X X Q, same
     // span) was measured to lose the tail of the spectrum in FP32 (eigenvalue errors ~0.9 at index r-1).
-    for (int o = 0; o < north; ++o) {
+    // Optional overlapped power iteration (RKFAC_OVERLAP_ORTH=1; default off).  The reference orthonormalises every
+    // product: Y' = X (Y L^-T), L = chol(Y^T Y) (rnla.hpp:47-56).  By associativity Y' = (X Y) L^-T, and X Y depends
+    // only on Y -- like the Gram and its Cholesky-inverse -- so the product can run NEXT to the latency-bound Gram +
+    // Cholesky-inverse (side stream) and one skinny product Z L^-T joins them.  Measured on B200:
+    // a lone 4609-wide layer's chain shortens, the 5-group VGG16 step gains 3 % (it is throughput-bound), and the
+    // rounding of the Gram coefficients is amplified by lambda_1 / lambda_j in column j (the reference's order keeps
+    // it inside the span of the earlier columns): the last Ritz values move by ~(6e-8 lambda_1 / lambda_r)^2, i.e.
+    // 2.8e-5 at VGG16's spectrum (bar met) but 1.2e-3 at config 5's (lambda_r / lambda_1 = 1.6e-6, bar missed; an
+    // FP64 Gram / Cholesky / Z L^-T restores 4e-5 but costs more than the overlap gains).  Hence off by default.
+    const bool overlap = overlap_orth_ && n_fp64_orth_ == 1 && north >= 3;
+    for (int o = 0; o < north && !(overlap && o >= 1); ++o) {
         const int y = cur_q ^ 1;
         timed_xq(y, o);
         last_fp64 = o < n_fp64_orth_;
@@ -684,6 +721,47 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
         // S[y] -> S[cur_q]; the row-major planes of Q are read only by the CholeskyQR2 pass and the lift
         orth(y, last_fp64, s, o == north - 1);
         mark(kOrth, false);
+    }
+    if (overlap) {
+        const int y = cur_q ^ 1;  // Y lives in S[y] throughout, Z in S[cur_q].R
+        const int n_over = std::max(0, north - 2 - explicit_tail_);
+        mark(kXQ, true);
+        (n_over == 0 ? xq_ : xq_tl_)[y]->launch(s);  // Y1 = X Q0
+        mark(kXQ, false);
+        // with stage timing on, the side chain is issued on the main stream (every stage timed alone)
+        cudaStream_t side = timing_ ? s : side_;
+        for (int o = 1; o <= n_over; ++o) {
+            if (side != s) {
+                RKFAC_CUDA(cudaEventRecord(ev_fork_, s));
+                RKFAC_CUDA(cudaStreamWaitEvent(side, ev_fork_, 0));
+            }
+            mark(kXQ, true);
+            xz_[cur_q]->launch(s);  // Z = X Y (row-major only)
+            mark(kXQ, false);
+            mark(kOrth, true);
+            gram_[y]->launch(side);
+            launch_cholinv(d_chol32_[y].as<CholDesc>(), n, wmax_, false, false, kTol32, side);
+            if (side != s) {
+                RKFAC_CUDA(cudaEventRecord(ev_join_, side));
+                RKFAC_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+            }
+            // Y' = Z L^-T back into S[y] (the last iterate with its row-major plane, for the explicit CholeskyQR2)
+            (o == n_over ? tri_ : tri_t_)[cur_q]->launch(s);
+            mark(kOrth, false);
+        }
+        // the last explicit_tail_ products in the reference's order (orthonormalise, then multiply)
+        for (int o = 0; o < std::min(explicit_tail_, std::max(0, north - 2)); ++o) {
+            mark(kOrth, true);
+            orth(y, false, s, false);
+            mark(kOrth, false);
+            mark(kXQ, true);
+            xq_[y]->launch(s);
+            mark(kXQ, false);
+        }
+        mark(kOrth, true);
+        orth(y, false, s, true);
+        mark(kOrth, false);
+        last_fp64 = false;
     }
     if (!last_fp64) {  // CholeskyQR2: second pass so the final basis is orthonormal to FP32 rounding
         mark(kOrth, true);

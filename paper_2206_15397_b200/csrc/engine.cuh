@@ -156,6 +156,8 @@ class Plan {
 
     // Stage objects, indexed by the role buffer they write (xq, core: Y in S[dir]) or read (orth: src).
     // xqf_: the final X*Q (input of the core) with short accumulation chains (see kSliceK in engine.cu)
+    // xq_tl_ / xz_: the overlapped power iteration's products (Y^T + lo plane only; Z row-major only)
+    std::unique_ptr<TcGemm> xq_tl_[2], xz_[2];
     std::unique_ptr<TcGemm> xq_[2], xq_t_[2], xqf_[2], gram_[2], tri_[2], tri_t_[2], core_[2], lift_[2];
     std::unique_ptr<Gram64Batch> gram64_[2];
     std::unique_ptr<Tri64Batch> tri64_[2];
@@ -177,6 +179,11 @@ class Plan {
     // orths give the same parity error, 0 gives eigenvalue errors of ~5e-2.
     int n_fp64_orth_ = 1;
     int tc_cap_ = 0;  // persistent tensor-core grid cap (0: all SMs)
+    // overlapped power iteration (decompose): Gram + Cholesky-inverse on side_ next to the product X Y
+    bool overlap_orth_ = false;  // opt-in (RKFAC_OVERLAP_ORTH=1): see decompose()
+    int explicit_tail_ = 1;  // trailing products kept in the reference's order
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
     bool timing_ = false;
     struct Rec { int kind; size_t b, e; };
