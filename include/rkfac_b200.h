@@ -165,6 +165,9 @@ int rkfac_plan_ea_update(rkfac_plan_t plan, double rho, double scale);
  * tag_f = f unless rkfac_plan_set_tags was called. */
 int rkfac_plan_decompose(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
 int rkfac_plan_set_tags(rkfac_plan_t plan, const uint64_t* tags);
+/* rkfac_plan_ea_update followed by rkfac_plan_decompose of the same step, as rkfac_plan_step runs them (Omega is
+ * generated next to the EA update); bitwise the two separate calls. */
+int rkfac_plan_ea_decompose(rkfac_plan_t plan, double rho, double scale, uint64_t rng_root, uint64_t step);
 /* All layers: outs = LEFT_G(RIGHT_A(grads)) (optimizer.hpp:159-162). */
 int rkfac_plan_precondition(rkfac_plan_t plan, double lambda);
 /* EA (if samples bound) -> decompose -> precondition (if layers bound) -> all-gather (if rkfac_plan_set_gather). */

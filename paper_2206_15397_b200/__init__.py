@@ -27,6 +27,10 @@ from typing import Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librkfac_b200.so")
+# A multi-group step runs on 2 streams per group (+ copy streams): with the driver's default of 8 hardware work queues
+# streams share queues and serialise falsely.  Read when the CUDA context is created, so it is set at import (a host
+# that already set it keeps its value); the library enables its side-stream overlap only when it sees >= 16.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 # ---------------------------------------------------------------------------------------------- errors
 
@@ -108,6 +112,7 @@ SIGNATURES = {
     "rkfac_plan_set_tags": (C.c_int, [_vp, C.POINTER(_c_u64)]),
     "rkfac_plan_ea_update": (C.c_int, [_vp, C.c_double, C.c_double]),
     "rkfac_plan_decompose": (C.c_int, [_vp, _c_u64, _c_u64]),
+    "rkfac_plan_ea_decompose": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64]),
     "rkfac_plan_precondition": (C.c_int, [_vp, C.c_double]),
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
@@ -561,6 +566,12 @@ class BatchedStep:
         _check(self.ctx.lib.rkfac_plan_decompose(self.h, _c_u64(rng_root), _c_u64(step)), self.ctx.h,
                "plan_decompose")
 
+    def ea_decompose(self, rng_root: int, step: int, rho: float = 0.95, scale: float = 1.0):
+        """ea_update + decompose of the same step (Omega generated next to the EA update; bitwise the two calls)."""
+        self.ctx.sync_stream()
+        _check(self.ctx.lib.rkfac_plan_ea_decompose(self.h, rho, scale, _c_u64(rng_root), _c_u64(step)), self.ctx.h,
+               "plan_ea_decompose")
+
     def precondition(self, lam: float):
         if lam <= 0.0:
             raise DampingNonpositive("apply_lowrank_damped_inverse: lambda must be > 0")
@@ -834,8 +845,9 @@ class StreamedStep:
                 last_samples.record(st)
                 mark(st, "samples_in", g)
                 if sub.samples:
-                    sub.ea_update(rho, scale)
-                sub.decompose(rng_root, step)
+                    sub.ea_decompose(rng_root, step, rho, scale)
+                else:
+                    sub.decompose(rng_root, step)
                 mark(st, "decomposed", g)
         # 2. the gradients, behind all the samples on the copy engine
         got_grads = {}

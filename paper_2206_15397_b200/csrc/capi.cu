@@ -368,6 +368,10 @@ int rkfac_plan_decompose(rkfac_plan_t plan, uint64_t root, uint64_t step) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->decompose(1, root, step); });
 }
 
+int rkfac_plan_ea_decompose(rkfac_plan_t plan, double rho, double scale, uint64_t root, uint64_t step) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->ea_decompose(rho, scale, root, step); });
+}
+
 int rkfac_plan_precondition(rkfac_plan_t plan, double lambda) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->precondition(lambda); });
 }

@@ -83,7 +83,14 @@ Plan::Plan(Context* ctx, const rkfac_factor_desc* descs, int n, int method) : ct
         RKFAC_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi_pri));
         RKFAC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         RKFAC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        RKFAC_CUDA(cudaEventCreateWithFlags(&ev_pre_, cudaEventDisableTiming));
+        RKFAC_CUDA(cudaEventCreateWithFlags(&ev_copy_, cudaEventDisableTiming));
     }
+    // The side stream doubles the streams of a multi-group step; with the driver's default of 8 hardware work queues
+    // streams then share queues and serialise falsely (measured: 5 groups eager 7.3 -> 11.0 ms), so the overlap is
+    // on only when the process raised CUDA_DEVICE_MAX_CONNECTIONS (the Python package sets 32 at import).
+    if (const char* mc = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) step_overlap_ = std::atoi(mc) >= 16;
+    if (const char* so = std::getenv("RKFAC_STEP_OVERLAP")) step_overlap_ = std::atoi(so) != 0;
     Carver c;
     struct Offs {
         size_t S[2][4], Xc, G64, G32, L64, L32, L32lo, flags, chol, core, esc, refl, tau, dvec, evec, evals,
@@ -178,6 +185,8 @@ Plan::~Plan() {
     for (auto& e : pool_) cudaEventDestroy(e);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_pre_) cudaEventDestroy(ev_pre_);
+    if (ev_copy_) cudaEventDestroy(ev_copy_);
     if (side_) cudaStreamDestroy(side_);
 }
 
@@ -677,7 +686,7 @@ void Plan::ea_update(double rho, double scale) {
     mark(kEA, false);
 }
 
-void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
+void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh, int flags) {
     RKFAC_REQUIRE(factors_bound_, RKFAC_INVALID_ARGUMENT, "factors not bound");
     cudaStream_t s = ctx_->stream;
     const int n = nfactors();
@@ -689,7 +698,8 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     mark(kDecompose, true);
     (void)x_lo_fresh;
     if (!x_tma_ok_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);  // padded TMA copy of X
-    launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
+    if (flags & kOmegaAhead) RKFAC_CUDA(cudaStreamWaitEvent(s, ev_pre_, 0));  // generated next to the EA update
+    else launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
     int cur_q = 1;  // the basis lives in S[cur_q]
     const int north = 2 * qmax + 1;
     bool last_fp64 = false;
@@ -783,12 +793,19 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh) {
     launch_post(d_post_.as<PostDesc>(), n, s);
     lift_[y]->launch(s);
     if (method_ == RKFAC_RSVD) launch_complete(d_complete_u_.as<CompleteDesc>(), n, s);
-    launch_copy(d_copy_ut_.as<CopyDesc>(), n, copy_ut_total_, s);
+    if (flags & kDeferUtCopy) {  // U^T leaves next to the preconditioning (which reads the plan's own copies)
+        RKFAC_CUDA(cudaEventRecord(ev_fork_, s));
+        RKFAC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        launch_copy(d_copy_ut_.as<CopyDesc>(), n, copy_ut_total_, side_);
+        RKFAC_CUDA(cudaEventRecord(ev_copy_, side_));
+    } else {
+        launch_copy(d_copy_ut_.as<CopyDesc>(), n, copy_ut_total_, s);
+    }
     mark(kEig, false);
     mark(kDecompose, false);
 }
 
-void Plan::precondition(double lambda) {
+void Plan::precondition(double lambda, bool j_copied) {
     RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
     RKFAC_REQUIRE(factors_bound_, RKFAC_INVALID_ARGUMENT, "factors not bound");
     if (layers_.empty()) return;
@@ -796,7 +813,8 @@ void Plan::precondition(double lambda) {
     cudaStream_t s = ctx_->stream;
     mark(kApply, true);
     launch_bracket(d_bracket_.as<BracketDesc>(), nfactors(), lambda, s);
-    launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, s);  // J -> aligned TMA copy
+    if (!j_copied)
+        launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, s);  // J -> aligned TMA copy
     for (auto& a : ap_) a->launch(s);
     mark(kApply, false);
 }
@@ -807,9 +825,24 @@ void Plan::prepare(double rho, double scale, double lambda) {
     if (!layers_.empty() && lambda != ap_lambda_) build_apply_stages(lambda);
 }
 
-void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double lambda) {
-    RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
-    mark(kStep, true);
+// The pieces of a step that depend on neither the EA update nor the decomposition run next to them on the side
+// stream: Omega (FP64 transcendental math: ~0.1 ms per VGG16 group) and, for step(), the aligned copy of the
+// gradients next to the EA update; U^T's copy-out next to the preconditioning.  Stage timing keeps everything in line.
+bool Plan::launch_ahead(uint64_t root, uint64_t stp, bool with_grads) {
+    if (!step_overlap_ || timing_ || nfactors() == 0) return false;
+    cudaStream_t s = ctx_->stream;
+    RKFAC_CUDA(cudaEventRecord(ev_fork_, s));
+    RKFAC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    launch_omega(d_omega_.as<OmegaDesc>(), nfactors(), omega_total_, 1, root, stp, side_);
+    if (with_grads && !layers_.empty())
+        launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, side_);
+    RKFAC_CUDA(cudaEventRecord(ev_pre_, side_));
+    return true;
+}
+
+void Plan::ea_decompose(double rho, double scale, uint64_t root, uint64_t stp) {
+    RKFAC_REQUIRE(factors_bound_, RKFAC_INVALID_ARGUMENT, "factors not bound");
+    const bool over = launch_ahead(root, stp, false);
     bool fresh = false;
     if (samples_bound_) {
         ea_update(rho, scale);
@@ -817,8 +850,24 @@ void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double la
         for (auto& F : f_) all = all && F.M && F.n > 0;
         fresh = ea_tc_ && all;
     }
-    decompose(1, root, stp, fresh);
-    precondition(lambda);
+    decompose(1, root, stp, fresh, over ? kOmegaAhead : 0);
+}
+
+void Plan::step(double rho, double scale, uint64_t root, uint64_t stp, double lambda) {
+    RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
+    RKFAC_REQUIRE(factors_bound_, RKFAC_INVALID_ARGUMENT, "factors not bound");
+    mark(kStep, true);
+    const bool over = launch_ahead(root, stp, true);
+    bool fresh = false;
+    if (samples_bound_) {
+        ea_update(rho, scale);
+        bool all = true;
+        for (auto& F : f_) all = all && F.M && F.n > 0;
+        fresh = ea_tc_ && all;
+    }
+    decompose(1, root, stp, fresh, over ? (kOmegaAhead | kDeferUtCopy) : 0);
+    precondition(lambda, over);
+    if (over) RKFAC_CUDA(cudaStreamWaitEvent(ctx_->stream, ev_copy_, 0));
     if (gathered_) gather();
     mark(kStep, false);
 }

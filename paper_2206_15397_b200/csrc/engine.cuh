@@ -108,8 +108,12 @@ class Plan {
 
     void ea_update(double rho, double scale);
     // mode 1: seeds from substream(root, step, tag); mode 0: explicit seeds.
-    void decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh = false);
-    void precondition(double lambda);
+    // flags / j_copied: set by step() and ea_decompose(), which run Omega (and the gradient copy) next to the EA update
+    enum DecompFlags { kOmegaAhead = 1, kDeferUtCopy = 2 };
+    void decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh = false, int flags = 0);
+    void precondition(double lambda, bool j_copied = false);
+    // EA update + decomposition of the same step (Omega generated next to the EA update)
+    void ea_decompose(double rho, double scale, uint64_t root, uint64_t step);
     void step(double rho, double scale, uint64_t root, uint64_t step, double lambda);
     // Multi-GPU (config 4): step() ends with packing this rank's layer outputs at offsets[l] of a chunk of chunk
     // floats and all-gathering the chunks over the context's NCCL communicator into gathered (nranks * chunk).
@@ -138,6 +142,7 @@ class Plan {
     void build_apply_stages(double lambda);
     void orth(int src, bool fp64, cudaStream_t s, bool need_r = true);
     void mark(int kind, bool begin);
+    bool launch_ahead(uint64_t root, uint64_t step, bool with_grads);
 
     Context* ctx_;
     int method_;
@@ -183,7 +188,8 @@ class Plan {
     bool overlap_orth_ = false;  // opt-in (RKFAC_OVERLAP_ORTH=1): see decompose()
     int explicit_tail_ = 1;  // trailing products kept in the reference's order
     cudaStream_t side_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_pre_ = nullptr, ev_copy_ = nullptr;
+    bool step_overlap_ = false;  // step(): Omega / gradient copy next to the EA update, U^T copy-out next to the apply
 
     bool timing_ = false;
     struct Rec { int kind; size_t b, e; };
