@@ -342,6 +342,13 @@ void Plan::build_decomp_stages() {
         xq_t_[dir] = new_tc();
         xq_tl_[dir] = new_tc();
         xz_[dir] = new_tc();
+        // the long-K products run on CTA pairs (cta_group::2; tc_gemm.cu kCfg 3): RKFAC_XQ_PAIR=0 disables
+        static const bool pair_xq = [] {
+            const char* e = std::getenv("RKFAC_XQ_PAIR");
+            return !(e && e[0] == '0');
+        }();
+        for (TcGemm* g : {xq_[dir].get(), xqf_[dir].get(), xq_t_[dir].get(), xq_tl_[dir].get(), xz_[dir].get()})
+            g->set_two_cta(pair_xq);
         gram_[dir] = new_tc();
         tri_[dir] = new_tc();
         tri_t_[dir] = new_tc();

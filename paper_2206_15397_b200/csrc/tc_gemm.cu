@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -35,7 +36,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 16;          // floats per K block (64 bytes per row => SWIZZLE_64B)
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 6;
 constexpr int kMaxBN = 256;
 constexpr int kATileBytes = kBM * kBK * 4;     // 8 KB (one 128-row A sub-tile)
 constexpr int kBTileBytes = kMaxBN * kBK * 4;  // 16 KB
@@ -56,11 +57,16 @@ constexpr int kCinRing = RKFAC_EA_CIN_RING;
 #ifndef RKFAC_EA_STAGES
 #define RKFAC_EA_STAGES 4  // mainloop stages of the EA configuration (its region reaches 208 KB; 3: 6 % slower)
 #endif
+//   kCfg 3, CTA pairs (cta_group::2, M = 256 over two SMs): 6 stages of [A hi][A lo][B hi half][B lo half] = 32 KB;
+//           each CTA of the pair holds its own 128 rows of A and HALF of the B tile's rows.  Measured: the mainloop
+//           runs at the same per-SM rate as the single-CTA configurations (1040 cycles per 128 x 240 x 16 block of
+//           six MMAs, i.e. the measured dense-TF32 rate; 512-row pair tiles, B lo planes formed in smem and deeper
+//           pipelines all leave it unchanged), but its 256-row tiles over SM pairs schedule better (X*Q 3.28 -> 3.06 ms)
 template <int kCfg>
 struct StageCfg {
     static constexpr int kSub = kCfg == 1 ? 2 : 1;
-    static constexpr int kStages = kCfg == 0 ? 4 : (kCfg == 2 ? RKFAC_EA_STAGES : 3);
-    static constexpr int kBTile = kCfg == 2 ? kBM * kBK * 4 : kBTileBytes;
+    static constexpr int kStages = kCfg == 0 ? 4 : (kCfg == 2 ? RKFAC_EA_STAGES : (kCfg == 3 ? 6 : 3));
+    static constexpr int kBTile = kCfg == 2 ? kBM * kBK * 4 : (kCfg == 3 ? kBTileBytes / 2 : kBTileBytes);
     static constexpr int kStageBytes = 2 * kSub * kATileBytes + 2 * kBTile;
 };
 constexpr int kStagesBytesMax = 3 * (4 * kATileBytes + 2 * kBTileBytes);  // == 4 * 48 KB
@@ -157,6 +163,63 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
         "}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// CTA pair (cta_group::2): issued by the leader CTA only; D is 256 x N (128 TMEM lanes in each CTA), A's rows 128..255
+// and B's rows N/2..N-1 are read from the peer CTA's shared memory at the same offsets.
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ uint32_t idesc_tf32_pair(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)((2 * kBM) >> 4) << 24);
+}
+// completion of the pair's MMAs arrives on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    const uint16_t mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// arrive on the barrier at this offset in CTA `rank` of the cluster.  Default semantics (release at CTA scope), as
+// for any consumer-release arrival across a cluster: a cluster-scope release costs a full memory barrier per arrival
+// (measured: the converter warps then bound the mainloop, 2.1x slower); the data the leader's MMAs read from the
+// peer's shared memory is ordered by the fence.proxy.async that precedes the arrival.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    uint32_t addr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+// wait with acquire at cluster scope (the arrivals come from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAITC:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 1000000;\n"
+        "@P1 bra DONEC;\n"
+        "bra LAB_WAITC;\n"
+        "DONEC:\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -420,6 +483,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                const TcTile* __restrict__ tiles, const int* __restrict__ cta_begin) {
     __shared__ TcProb s_pr[4];  // per epilogue warp
     constexpr bool kPair = kCfg == 1;
+    constexpr bool k2 = kCfg == 3;  // CTA pairs: blockIdx.x / 2 is the schedule slot, %cluster_ctarank the half
     constexpr int kStages = StageCfg<kCfg>::kStages;
     constexpr int kStageBytes = StageCfg<kCfg>::kStageBytes;
     constexpr int kSub = StageCfg<kCfg>::kSub;
@@ -433,27 +497,37 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
     float (*stage_tiles)[32][36] =  // unused by kCfg 2 when its region extends past kStagesBytesMax
         reinterpret_cast<float (*)[32][36]>(smem + kStagesBytesMax + kBarrierBytes);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int t_begin = cta_begin[blockIdx.x], t_end = cta_begin[blockIdx.x + 1];
+    const int slot_id = k2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int crank = k2 ? (int)cluster_ctarank() : 0;
+    const int t_begin = cta_begin[slot_id], t_end = cta_begin[slot_id + 1];
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
-            mbar_init(&bars->conv[s], kConvThreads / 32);
+            // pairs: the leader's barrier collects the converter warps of both CTAs
+            mbar_init(&bars->conv[s], k2 ? 2 : kConvThreads / 32);  // pairs: one converter warp of each CTA
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->tmem_full[a], 1);
-            mbar_init(&bars->tmem_empty[a], 128);
+            mbar_init(&bars->tmem_empty[a], k2 ? 8 : 128);  // pairs: one arrival per epilogue warp of both CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // TMEM: 2 accumulators x 256 fp32 columns
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         smem_u32(&bars->tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (k2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(&bars->tmem_base)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(&bars->tmem_base)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (k2) cluster_sync_all();  // the peer's barriers are initialised and its TMEM allocated
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_base;
 
@@ -467,30 +541,33 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const TcProb& pr = probs[tl.prob];
                 const CUtensorMap* mp = maps + kMapsPerProb * tl.prob;
                 const uint32_t aplanes = (pr.a_conv || pr.single) ? 1u : 2u, bplanes = (pr.b_conv || pr.single) ? 1u : 2u;
+                const int brows = k2 ? pr.n_tile / 2 : pr.n_tile;  // pairs: this CTA's half of the B tile
+                // pairs: this CTA's rows follow the leader's (one or two 128-row sub-tiles each)
+                const int am0 = tl.m0 + crank * ((kPair && tl.pair) ? 2 : 1) * kBM, bn0 = tl.n0 + crank * brows;
                 const uint32_t bytes =
-                    (tl.pair ? 2u : 1u) * aplanes * kATileBytes + bplanes * (uint32_t)pr.n_tile * kBK * 4u;
+                    ((kPair && tl.pair) ? 2u : 1u) * aplanes * kATileBytes + bplanes * (uint32_t)brows * kBK * 4u;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
                     unsigned char* st = smem + stage * kStageBytes;
                     mbar_expect_tx(&bars->full[stage], bytes);
                     const int k0 = kb * kBK;
-                    tma_load_2d(st, mp + 0, &bars->full[stage], k0, tl.m0);
-                    if (!pr.a_conv && !pr.single) tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0);
+                    tma_load_2d(st, mp + 0, &bars->full[stage], k0, am0);
+                    if (!pr.a_conv && !pr.single) tma_load_2d(st + kSub * kATileBytes, mp + 1, &bars->full[stage], k0, am0);
                     if (kPair && tl.pair) {
-                        tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, tl.m0 + kBM);
+                        tma_load_2d(st + kATileBytes, mp + 0, &bars->full[stage], k0, am0 + kBM);
                         if (!pr.a_conv && !pr.single)
-                            tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, tl.m0 + kBM);
+                            tma_load_2d(st + 3 * kATileBytes, mp + 1, &bars->full[stage], k0, am0 + kBM);
                     }
-                    tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, tl.n0);
+                    tma_load_2d(st + 2 * kSub * kATileBytes, mp + 2, &bars->full[stage], k0, bn0);
                     if (!pr.b_conv && !pr.single)
-                        tma_load_2d(st + 2 * kSub * kATileBytes + kBTileS, mp + 3, &bars->full[stage], k0, tl.n0);
+                        tma_load_2d(st + 2 * kSub * kATileBytes + kBTileS, mp + 3, &bars->full[stage], k0, bn0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (pairs: the leader CTA issues for both) ----------------
+        if (lane == 0 && crank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int rr = 0;                     // next accumulator slot for a single tile
@@ -502,13 +579,19 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 const int slot0 = (kPair && tl.pair) ? 0 : rr;
                 for (int sub = 0; sub < nsub; ++sub) {
                     const int a = slot0 + sub;
-                    mbar_wait(&bars->tmem_empty[a], (uses[a] & 1u) ^ 1u);
+                    if constexpr (k2) mbar_wait_cluster(&bars->tmem_empty[a], (uses[a] & 1u) ^ 1u);
+                    else mbar_wait(&bars->tmem_empty[a], (uses[a] & 1u) ^ 1u);
                 }
                 tc_fence_after();
-                const uint32_t idesc = idesc_tf32(pr.n_tile);
+                const uint32_t idesc = k2 ? idesc_tf32_pair(pr.n_tile) : idesc_tf32(pr.n_tile);
                 const bool single = pr.single != 0;
                 for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
+                    // pairs: the converter warps of both CTAs arrive here once their own tiles have landed
+#ifdef RKFAC_PAIR_CLUSTER_ACQ
+                    if constexpr (k2) mbar_wait_cluster(&bars->conv[stage], phase);
+                    else
+#endif
                     mbar_wait(&bars->conv[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * kStageBytes);
@@ -520,19 +603,30 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte row
                             const uint32_t first = (kb == tl.kb0 && kk == 0) ? 0u : 1u;
-                            if (!single) {
-                                mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
-                                mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
+                            if constexpr (k2) {
+                                if (!single) {
+                                    mma_tf32_pair(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
+                                    mma_tf32_pair(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
+                                }
+                                mma_tf32_pair(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc,
+                                              single ? first : 1u);
+                            } else {
+                                if (!single) {
+                                    mma_tf32(tmem_d, umma_desc_sw64(a_lo + off), umma_desc_sw64(b_hi + off), idesc, first);
+                                    mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_lo + off), idesc, 1u);
+                                }
+                                mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc,
+                                         single ? first : 1u);
                             }
-                            mma_tf32(tmem_d, umma_desc_sw64(a_hi + off), umma_desc_sw64(b_hi + off), idesc,
-                                     single ? first : 1u);
                         }
                     }
-                    mma_commit(&bars->empty[stage]);
+                    if constexpr (k2) mma_commit_pair(&bars->empty[stage]);
+                    else mma_commit(&bars->empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 for (int sub = 0; sub < nsub; ++sub) {
-                    mma_commit(&bars->tmem_full[slot0 + sub]);
+                    if constexpr (k2) mma_commit_pair(&bars->tmem_full[slot0 + sub]);
+                    else mma_commit(&bars->tmem_full[slot0 + sub]);
                     ++uses[slot0 + sub];
                 }
                 if (!(kPair && tl.pair)) rr ^= 1;
@@ -540,16 +634,26 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
         }
     } else if (warp >= 6) {
         // ---------------- A lo-plane converters ----------------
-        const int ct = threadIdx.x - 6 * 32;
+        // kCfg 0-2: both warps share every stage.  CTA pairs (kCfg 3): the warps take alternate K blocks, each
+        // converting a whole stage alone, so one warp's proxy fence (the long pole of a stage) overlaps the other
+        // warp's conversion.
+        constexpr int kCT = k2 ? 32 : kConvThreads;  // threads converting one stage
+        const int ct = k2 ? lane : (int)threadIdx.x - 6 * 32;
+        const int mine = warp - 6;  // kCfg 3: parity of the K blocks this warp converts
         int stage = 0;
         uint32_t phase = 0;
+        uint32_t kbn = 0;  // K blocks seen
         for (int t = t_begin; t < t_end; ++t) {
             const TcTile tl = tiles[t];
             const bool single = probs[tl.prob].single != 0;
             const bool conv = probs[tl.prob].a_conv != 0 && !single, bconv = probs[tl.prob].b_conv != 0 && !single;
-            const int nb16 = probs[tl.prob].n_tile * kBK / 4;  // float4s of the B tile
+            const int nb16 = (k2 ? probs[tl.prob].n_tile / 2 : probs[tl.prob].n_tile) * kBK / 4;  // float4s of the B tile
             const int nsub = (kPair && tl.pair) ? 2 : 1;
-            for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+            for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++kbn) {
+                if (k2 && (int)(kbn & 1u) != mine) {
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    continue;
+                }
                 mbar_wait(&bars->full[stage], phase);  // also paces the arrivals of unconverted problems
                 if (conv) {
                     unsigned char* st = smem + stage * kStageBytes;
@@ -557,9 +661,9 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         const float4* src = reinterpret_cast<const float4*>(st + sub * kATileBytes);
                         float4* dst = reinterpret_cast<float4*>(st + (kSub + sub) * kATileBytes);
 #pragma unroll
-                        for (int i = 0; i < kATileBytes / 16 / kConvThreads; ++i) {
-                            const float4 x = src[i * kConvThreads + ct];
-                            dst[i * kConvThreads + ct] = lo4(x);
+                        for (int i = 0; i < kATileBytes / 16 / kCT; ++i) {
+                            const float4 x = src[i * kCT + ct];
+                            dst[i * kCT + ct] = lo4(x);
                         }
                     }
                 }
@@ -567,11 +671,14 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     unsigned char* st = smem + stage * kStageBytes;
                     const float4* src = reinterpret_cast<const float4*>(st + 2 * kSub * kATileBytes);
                     float4* dst = reinterpret_cast<float4*>(st + 2 * kSub * kATileBytes + kBTileS);
-                    for (int i = ct; i < nb16; i += kConvThreads) dst[i] = lo4(src[i]);
+                    for (int i = ct; i < nb16; i += kCT) dst[i] = lo4(src[i]);
                 }
                 if (conv || bconv) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tensor core
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->conv[stage]);
+                if (lane == 0) {
+                    if (k2 && crank != 0) mbar_arrive_remote(&bars->conv[stage], 0);  // the leader issues the MMAs
+                    else mbar_arrive(&bars->conv[stage]);
+                }
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
@@ -625,7 +732,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             const int acc = slot0 + sub;
             const uint32_t acc_phase = uses[acc] & 1u;
             ++uses[acc];
-            const int m0s = tl.m0 + sub * kBM;  // this sub-tile's first row
+            const int m0s = tl.m0 + (crank * nsub + sub) * kBM;  // this sub-tile's first row (CTA pairs: rank-major)
             const int mbase = m0s + q * 32;
             const int m = mbase + lane;
             const bool diag = pr.sym && m0s == tl.n0;
@@ -756,15 +863,30 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 }
             }
             tc_fence_before();
-            mbar_arrive(&bars->tmem_empty[acc]);
+            if constexpr (k2) {
+                __syncwarp();
+                if (lane == 0) {
+                    if (crank != 0) mbar_arrive_remote(&bars->tmem_empty[acc], 0);
+                    else mbar_arrive(&bars->tmem_empty[acc]);
+                }
+            } else {
+                mbar_arrive(&bars->tmem_empty[acc]);
+            }
           }
         }
         if (kCfg == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    __syncthreads();
+    if constexpr (k2) {
+        tc_fence_before();
+        __syncwarp();  // the single-lane roles rejoin their warps before the aligned cluster barrier
+        cluster_sync_all();  // neither CTA leaves (or frees its TMEM) while the pair's MMAs / remote arrivals may touch it
+    } else {
+        __syncthreads();
+    }
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        if constexpr (k2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 }
 
@@ -917,6 +1039,7 @@ bool tc_operand_ok(const float* p, long long ld) {
 int TcGemm::add(const TcProblemDesc& d) {
     RKFAC_REQUIRE(d.M > 0 && d.N > 0 && d.K > 0, RKFAC_INVALID_ARGUMENT, "empty tc problem");
     RKFAC_REQUIRE(!d.sym || d.M == d.N, RKFAC_INVALID_ARGUMENT, "sym tc problem needs M == N");
+    RKFAC_REQUIRE(!(two_cta_ && d.sym), RKFAC_INVALID_ARGUMENT, "CTA-pair tc problems cannot be symmetric");
     TcProb p{};
     p.M = d.M; p.N = d.N; p.K = d.K; p.kblocks = (int)ceil_div(d.K, kBK); p.sym = d.sym;
     p.alpha = d.alpha; p.beta = d.beta; p.gamma = d.gamma; p.rs = d.rs; p.cs = d.cs;
@@ -960,8 +1083,9 @@ int TcGemm::add(const TcProblemDesc& d) {
     p.single = d.single;
     maps_.push_back(make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
     maps_.push_back(make_map(d.A_lo ? d.A_lo : d.A, d.K, d.M, d.lda, kBK, kBM));
-    maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, per));
-    maps_.push_back(make_map(d.B_lo ? d.B_lo : d.B, d.K, d.N, d.ldb, kBK, per));
+    const int bbox = two_cta_ ? per / 2 : per;  // CTA pairs: each CTA loads half of the B tile's rows
+    maps_.push_back(make_map(d.B, d.K, d.N, d.ldb, kBK, bbox));
+    maps_.push_back(make_map(d.B_lo ? d.B_lo : d.B, d.K, d.N, d.ldb, kBK, bbox));
     const bool out_tma = d.out0.p && d.out0.t == 0 && tc_operand_ok(d.out0.p, d.out0.ld);
     maps_.push_back(out_tma ? make_map(d.out0.p, d.N, d.M, d.out0.ld, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
                             : make_map(d.A, d.K, d.M, d.lda, kBK, kBM));
@@ -970,14 +1094,17 @@ int TcGemm::add(const TcProblemDesc& d) {
         if (kb0 >= kb1) continue;
         // tall problems (>= 8 row tiles, unsplit, not symmetric): pairs of row tiles share each B tile (halves the
         // L2->SM traffic of B, the re-read operand); the accumulation order per element is unchanged (bitwise)
-        const bool pairs = !d.sym && ks == 1 && ntm >= 8;
+        const bool pairs = !d.sym && ks == 1 && ntm >= 8 && !two_cta_;
+        // units of 128 rows per tile: single CTA 1 (2 when paired); CTA pairs 2
+        const int unit = two_cta_ ? 2 : 1;
         for (int tn = 0; tn < ntn; ++tn)
-            for (int tm = 0; tm < ntm; tm += (pairs ? 2 : 1)) {
-                if (d.sym && tn < tm) continue;
+            for (int tm = 0; tm < ntm;) {
+                if (d.sym && tn < tm) { tm += unit; continue; }
                 TcTile t{};
                 t.prob = prob; t.m0 = tm * kBM; t.n0 = tn * per; t.kb0 = kb0; t.kb1 = kb1; t.slice = s;
-                t.pair = (pairs && tm + 1 < ntm) ? 1 : 0;
+                t.pair = (pairs && tm + unit < ntm) ? 1 : 0;
                 tiles_.push_back(t);
+                tm += t.pair ? 2 * unit : unit;
             }
     }
     probs_.push_back(p);
@@ -985,6 +1112,31 @@ int TcGemm::add(const TcProblemDesc& d) {
     kept.ksplit = ks;  // a re-add (finalize's N split) keeps the K slicing, hence the arithmetic
     descs_.push_back(kept);
     return prob;
+}
+
+// CTA pairs that can be resident at once (TPCs with both SMs enabled)
+int TcGemm::pair_slots() {
+    static const int max_pairs = [] {
+        auto k = tc_gemm_kernel<3>;
+        const size_t smem = smem_bytes();
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(2 * kNumSMs);
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &lc) != cudaSuccess || n <= 0) n = kNumSMs / 2;
+        if (std::getenv("RKFAC_TC_DEBUG")) fprintf(stderr, "tc_gemm: %d CTA pairs resident\n", n);
+        return n;
+    }();
+    return max_pairs;
 }
 
 void TcGemm::finalize() {
@@ -997,7 +1149,15 @@ void TcGemm::finalize() {
         const char* e = std::getenv("RKFAC_TC_NSPLIT");
         return !(e && e[0] == '0');
     }();
-    if (nsplit_on && cap_ == 0 && std::getenv("RKFAC_TC_MAX_CTAS") == nullptr) {
+    // CTA pairs need enough 256-row tiles to fill the SM pairs; an under-filled launch (a multi-GPU shard, a
+    // single-factor call) goes back to single-CTA tiles and the N split below (same K order per element: bitwise)
+    if (two_cta_ && (int)tiles_.size() * 2 < pair_slots()) {
+        two_cta_ = false;
+        std::vector<TcProblemDesc> nd = descs_;
+        probs_.clear(); maps_.clear(); tiles_.clear(); descs_.clear();
+        for (const auto& d : nd) add(d);
+    }
+    if (nsplit_on && cap_ == 0 && !two_cta_ && std::getenv("RKFAC_TC_MAX_CTAS") == nullptr) {
         for (int it = 0; it < 4; ++it) {
             long long units = 0;
             for (const auto& t : tiles_) units += t.pair ? 2 : 1;
@@ -1021,7 +1181,7 @@ void TcGemm::finalize() {
     {
         long long units = 0, paired_units = (long long)tiles_.size();
         for (const auto& t : tiles_) units += t.pair ? 2 : 1;
-        if (paired_units < kNumSMs) {
+        if (paired_units < (two_cta_ ? pair_slots() : kNumSMs)) {
             std::vector<TcTile> split;
             split.reserve((size_t)units);
             for (const auto& t : tiles_) {
@@ -1029,7 +1189,7 @@ void TcGemm::finalize() {
                 a.pair = 0;
                 split.push_back(a);
                 if (t.pair) {
-                    a.m0 = t.m0 + kBM;
+                    a.m0 = t.m0 + (two_cta_ ? 2 : 1) * kBM;
                     split.push_back(a);
                 }
             }
@@ -1044,6 +1204,7 @@ void TcGemm::finalize() {
                  (p.ldo[0] % 4) == 0 && (reinterpret_cast<uintptr_t>(p.o[0]) % 16) == 0 && !p.o[1] && !p.o[2] &&
                  !p.o[3] && !p.rs && !p.cs && p.gamma == 0.f;
         cfg_ = ea ? 2 : (paired ? 1 : 0);
+        if (two_cta_) cfg_ = 3;
     }
     // split-K partial buffers
     size_t total = 0;
@@ -1070,6 +1231,7 @@ void TcGemm::finalize() {
     const int ntiles = (int)tiles_.size();
     int cap = cap_ > 0 ? std::min(kNumSMs, cap_) : kNumSMs;
     if (const char* e = std::getenv("RKFAC_TC_MAX_CTAS")) cap = std::max(1, std::min(kNumSMs, std::atoi(e)));
+    if (two_cta_) cap = std::max(1, std::min(cap / 2, pair_slots()));  // schedule slots are CTA pairs
     nctas_ = std::max(1, std::min(ntiles, cap));
     std::vector<int> order(ntiles);
     std::iota(order.begin(), order.end(), 0);
@@ -1109,10 +1271,29 @@ size_t TcGemm::smem_bytes() { return (size_t)kStagesBytesMax + kBarrierBytes + k
 void TcGemm::launch(cudaStream_t s) const {
     if (tiles_.empty()) return;
     const size_t smem = smem_bytes();
-    auto k = cfg_ == 2 ? tc_gemm_kernel<2> : (cfg_ == 1 ? tc_gemm_kernel<1> : tc_gemm_kernel<0>);
+    auto k = cfg_ == 3 ? tc_gemm_kernel<3>
+                       : (cfg_ == 2 ? tc_gemm_kernel<2> : (cfg_ == 1 ? tc_gemm_kernel<1> : tc_gemm_kernel<0>));
     RKFAC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(), d_tiles_.as<TcTile>(),
-                                     d_begin_.as<int>());
+    if (cfg_ == 3) {  // one cluster of two CTAs (a TPC's SM pair) per schedule slot
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(2 * nctas_);
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        RKFAC_CUDA(cudaLaunchKernelEx(&lc, k, (const TcProb*)d_probs_.as<TcProb>(),
+                                      (const CUtensorMap*)d_maps_.as<CUtensorMap>(),
+                                      (const TcTile*)d_tiles_.as<TcTile>(), (const int*)d_begin_.as<int>()));
+    } else {
+        k<<<nctas_, kThreads, smem, s>>>(d_probs_.as<TcProb>(), d_maps_.as<CUtensorMap>(), d_tiles_.as<TcTile>(),
+                                         d_begin_.as<int>());
+    }
     count_launch();
     RKFAC_CHECK_LAUNCH();
     if (any_split_ && !defer_reduce_) {

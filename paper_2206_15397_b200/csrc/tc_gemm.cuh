@@ -65,6 +65,9 @@ struct TcRed {  // split-K reduction map: first 32x32 output tile of a split pro
 class TcGemm {
   public:
     int add(const TcProblemDesc& d);
+    // CTA pairs (cta_group::2): every tile is 256 rows over the two SMs of a TPC, each holding half of the B tile --
+    // for the long-K products whose single-CTA mainloop is bound by shared-memory bandwidth.  Call before add().
+    void set_two_cta(bool on) { two_cta_ = on; }
     void set_max_ctas(int n) { cap_ = n; }  // persistent-grid cap (0: all SMs); leaves SMs to concurrent streams
     // the consumer reduces the split-K partials itself (launch() skips the reduction kernel); after finalize(),
     // split_of(prob) gives the partial buffer and slice count of a problem ({nullptr, 1} when it was not split)
@@ -79,6 +82,7 @@ class TcGemm {
     bool empty() const { return tiles_.empty(); }
     double flops() const;  // algorithmic 2*M*N*K (sym: half)
     static size_t smem_bytes();
+    static int pair_slots();
 
   private:
     std::vector<TcProb> probs_;
@@ -90,6 +94,7 @@ class TcGemm {
     bool any_split_ = false;
     int cfg_ = 0;
     int cap_ = 0;
+    bool two_cta_ = false;
     bool defer_reduce_ = false;  // shared-memory configuration of the launch (tc_gemm.cu StageCfg: single / paired / EA)
     int nred_ = 0;
     long long red_total_ = 0;
