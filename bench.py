@@ -485,7 +485,7 @@ def run_ours(args, wl):
 
     def one_step():
         if graph is not None:
-            graph.replay()
+            graph.replay(OMEGA_ROOT, 0)  # the step id is a replay-time input (rkfac_plan_set_step_seed)
         else:
             step.step(OMEGA_ROOT, 0, lam, 0.95, 1.0)
         gather()
@@ -591,7 +591,7 @@ def run_ours(args, wl):
         # stream, then precondition -> results D2H (one group's copies overlap the other group's kernels), replayed
         # as one CUDA graph (rk.HostStepGraph: the host enqueue of ~100 copies / launches leaves the critical path)
         if hgraph is not None:
-            hgraph.replay()
+            hgraph.replay(OMEGA_ROOT, 0)
         else:
             step.step_host(OMEGA_ROOT, 0, lam, h_samples, h_grads, h_outs, 0.95, 1.0)
         gather()
@@ -656,6 +656,7 @@ def run_ours(args, wl):
                        "oversampling": p, "power_iters": q, "lambda": lam, "n": n, "method": "srevd",
                        "parallelism": f"layer-LPT x{world}" + (" + NCCL all-gather" if world > 1 else " (no collective on one GPU)"),
                        "streams_per_gpu": args.groups,
+                       "cuda_graph": bool(args.graph),
                        "l2": f"inputs ({sum(4 * d * d for a, g in layers for d in (a, g)) / 1e6:.0f} MB of factors) "
                              "exceed the 126 MB L2; no flush",
                        "value_def": "factors inverted per second of the whole step (EA + rand-EVD + precondition "
@@ -707,8 +708,9 @@ def main():
     ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--e2e-graph", action=argparse.BooleanOptionalAction, default=True,
                     help="replay the host-buffer e2e step as one CUDA graph (rk.HostStepGraph)")
-    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=False,
-                    help="replay the timed step as one CUDA graph (rk.StepGraph); measured within 0.5 %% of eager")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="replay the timed step as one CUDA graph (rk.StepGraph: ~320 launches on 10 streams become "
+                         "one graph launch; the Omega step id is a replay-time input); --no-graph times eager calls")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

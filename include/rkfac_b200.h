@@ -202,8 +202,11 @@ int rkfac_plan_gather(rkfac_plan_t plan);
  * 4 orthonormalisations, 5 core + eigensolve + lift, 6 whole step. */
 int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
 /* Build every stage rkfac_plan_step(rho, scale, *, *, lambda) uses without launching anything, so the step only
- * enqueues kernels and may be captured into a CUDA graph (the Omega seed is a kernel argument: capture per step id). */
+ * enqueues kernels and may be captured into a CUDA graph.  A captured step reads (rng_root, step) from a pinned host
+ * pair at every replay: rkfac_plan_set_step_seed before the replay gives that replay its Omega (optimizer.hpp:189:
+ * the reference draws a fresh substream per step), so one graph serves every step id. */
 int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambda);
+int rkfac_plan_set_step_seed(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
 /* Cap the persistent tensor-core grids of this plan at `ctas` CTAs (0: one per SM), leaving SMs to the
  * latency-bound per-factor kernels of plans running concurrently on other streams (StreamedStep). */
 int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas);

@@ -113,6 +113,7 @@ SIGNATURES = {
     "rkfac_plan_ea_update": (C.c_int, [_vp, C.c_double, C.c_double]),
     "rkfac_plan_decompose": (C.c_int, [_vp, _c_u64, _c_u64]),
     "rkfac_plan_ea_decompose": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64]),
+    "rkfac_plan_set_step_seed": (C.c_int, [_vp, _c_u64, _c_u64]),
     "rkfac_plan_precondition": (C.c_int, [_vp, C.c_double]),
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
@@ -585,6 +586,11 @@ class BatchedStep:
         _check(self.ctx.lib.rkfac_plan_step(self.h, rho, scale, _c_u64(rng_root), _c_u64(step), lam), self.ctx.h,
                "plan_step")
 
+    def set_step_seed(self, rng_root: int, step: int):
+        """(rng_root, step) of the next replay of a CUDA graph captured from this plan's step / decomposition."""
+        _check(self.ctx.lib.rkfac_plan_set_step_seed(self.h, _c_u64(rng_root), _c_u64(step)), self.ctx.h,
+               "plan_set_step_seed")
+
     def prepare(self, lam: float, rho: float = 0.95, scale: float = 1.0):
         """Build every stage step(lam, rho, scale) uses, without launching (so the step can be graph-captured)."""
         if lam <= 0.0:
@@ -639,8 +645,8 @@ class StepGraph:
     """One full preconditioned step (EA -> rand-EVD -> precondition of every layer, every group's stream) captured
     once as a CUDA graph and replayed: ~70 dependent launches per group chain are submitted as one graph launch, so the
     inter-kernel gaps and the host enqueue cost leave the step.  Stages are built by ``prepare`` first (capture only
-    enqueues kernels); the Omega seeds (rng_root, step) are baked in, so capture one graph per step id (or reuse one
-    when the step id is fixed, as in bench.py).  Replays read the current contents of the step's device buffers
+    enqueues kernels); the Omega seeds (rng_root, step) are read at replay time (``replay(rng_root, step)``), so one
+    graph serves every step of a training run.  Replays read the current contents of the step's device buffers
     (factors, samples, grads) and are bitwise identical to ``step_obj.step``.
     """
 
@@ -660,7 +666,11 @@ class StepGraph:
         torch.cuda.current_stream(dev).wait_stream(s)
         self.launches = step_obj.ctx.launches() - n0  # kernels per replay
 
-    def replay(self):
+    def replay(self, rng_root: Optional[int] = None, step: Optional[int] = None):
+        """Replay the captured step; (rng_root, step), when given, select this replay's Omega substreams (the captured
+        step reads them from a pinned host pair: rkfac_plan_set_step_seed), else the pair of the last replay."""
+        if rng_root is not None:
+            self.step_obj.set_step_seed(rng_root, step)
         self.graph.replay()
 
 
@@ -689,7 +699,9 @@ class HostStepGraph:
         torch.cuda.current_stream(dev).wait_stream(s)
         self.launches = step_obj.ctx.launches() - n0
 
-    def replay(self):
+    def replay(self, rng_root: Optional[int] = None, step: Optional[int] = None):
+        if rng_root is not None:
+            self.step_obj.set_step_seed(rng_root, step)
         self.graph.replay()
 
 
@@ -800,6 +812,10 @@ class StreamedStep:
     def prepare(self, lam: float, rho: float = 0.95, scale: float = 1.0):
         for sub in self.subs:
             sub.prepare(lam, rho, scale)
+
+    def set_step_seed(self, rng_root: int, step: int):
+        for sub in self.subs:
+            sub.set_step_seed(rng_root, step)
 
     def step_host(self, rng_root: int, step: int, lam: float, h_samples, h_grads, h_outs, rho: float = 0.95,
                   scale: float = 1.0, timeline: Optional[list] = None):

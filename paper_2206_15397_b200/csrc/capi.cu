@@ -388,6 +388,10 @@ int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambd
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->prepare(rho, scale, lambda); });
 }
 
+int rkfac_plan_set_step_seed(rkfac_plan_t plan, uint64_t root, uint64_t step) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_step_seed(root, step); });
+}
+
 int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas) {
     return guarded(plan ? plan->ctx : nullptr, [&] {
         RKFAC_REQUIRE(ctas >= 0, RKFAC_INVALID_ARGUMENT, "negative CTA cap");

@@ -188,6 +188,7 @@ Plan::~Plan() {
     if (ev_pre_) cudaEventDestroy(ev_pre_);
     if (ev_copy_) cudaEventDestroy(ev_copy_);
     if (side_) cudaStreamDestroy(side_);
+    if (h_seed_) cudaFreeHost(h_seed_);
 }
 
 double Plan::xq_flops() const {
@@ -706,7 +707,8 @@ void Plan::decompose(int mode, uint64_t root, uint64_t step, bool x_lo_fresh, in
     (void)x_lo_fresh;
     if (!x_tma_ok_) launch_split(d_split_x_.as<SplitDesc>(), n, split_x_total_, s);  // padded TMA copy of X
     if (flags & kOmegaAhead) RKFAC_CUDA(cudaStreamWaitEvent(s, ev_pre_, 0));  // generated next to the EA update
-    else launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s);
+    else launch_omega(d_omega_.as<OmegaDesc>(), n, omega_total_, mode, root, step, s,
+                      mode == 1 ? captured_seed(root, step, s) : nullptr);
     int cur_q = 1;  // the basis lives in S[cur_q]
     const int north = 2 * qmax + 1;
     bool last_fp64 = false;
@@ -830,17 +832,40 @@ void Plan::prepare(double rho, double scale, double lambda) {
     RKFAC_REQUIRE(lambda > 0.0, RKFAC_DAMPING_NONPOSITIVE, "apply_lowrank_damped_inverse: lambda must be > 0");
     if (samples_bound_ && (rho != ea_rho_ || scale != ea_scale_)) build_ea_stage(rho, scale);
     if (!layers_.empty() && lambda != ap_lambda_) build_apply_stages(lambda);
+    if (!h_seed_) set_step_seed(0, 0);  // allocated here: no allocation while a stream is being captured
 }
 
 // The pieces of a step that depend on neither the EA update nor the decomposition run next to them on the side
 // stream: Omega (FP64 transcendental math: ~0.1 ms per VGG16 group) and, for step(), the aligned copy of the
 // gradients next to the EA update; U^T's copy-out next to the preconditioning.  Stage timing keeps everything in line.
+// While the stream is being captured into a CUDA graph, (root, step) go through a pinned host pair that a copy node
+// brings to the device at every replay, so one captured step serves every step id: rkfac_plan_set_step_seed before the
+// replay.  Eager launches pass them as kernel arguments (returns nullptr).
+const uint64_t* Plan::captured_seed(uint64_t root, uint64_t stp, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    RKFAC_CUDA(cudaStreamIsCapturing(s, &st));
+    if (st != cudaStreamCaptureStatusActive) return nullptr;
+    set_step_seed(root, stp);
+    RKFAC_CUDA(cudaMemcpyAsync(d_seed_.p, h_seed_, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    return d_seed_.as<uint64_t>();
+}
+
+void Plan::set_step_seed(uint64_t root, uint64_t stp) {
+    if (!h_seed_) {
+        RKFAC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_seed_), 2 * sizeof(uint64_t), cudaHostAllocDefault));
+        d_seed_.alloc(2 * sizeof(uint64_t));
+    }
+    h_seed_[0] = root;
+    h_seed_[1] = stp;
+}
+
 bool Plan::launch_ahead(uint64_t root, uint64_t stp, bool with_grads) {
     if (!step_overlap_ || timing_ || nfactors() == 0) return false;
     cudaStream_t s = ctx_->stream;
     RKFAC_CUDA(cudaEventRecord(ev_fork_, s));
     RKFAC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-    launch_omega(d_omega_.as<OmegaDesc>(), nfactors(), omega_total_, 1, root, stp, side_);
+    launch_omega(d_omega_.as<OmegaDesc>(), nfactors(), omega_total_, 1, root, stp, side_,
+                 captured_seed(root, stp, side_));
     if (with_grads && !layers_.empty())
         launch_split(d_split_j_.as<SplitDesc>(), (int)layers_.size(), split_j_total_, side_);
     RKFAC_CUDA(cudaEventRecord(ev_pre_, side_));

@@ -122,6 +122,8 @@ class Plan {
     // Builds every stage a step with these parameters uses (descriptor uploads), so that the step itself only
     // enqueues kernels and can be captured into a CUDA graph.
     void prepare(double rho, double scale, double lambda);
+    // (root, step) of the next replay of a captured step / decomposition (see captured_seed in engine.cu)
+    void set_step_seed(uint64_t root, uint64_t step);
 
     enum TimingKind { kEA = 0, kDecompose = 1, kApply = 2, kXQ = 3, kOrth = 4, kEig = 5, kStep = 6, kTimingKinds = 7 };
     void set_timing(bool on) { timing_ = on; timing_reset(); }
@@ -143,6 +145,7 @@ class Plan {
     void orth(int src, bool fp64, cudaStream_t s, bool need_r = true);
     void mark(int kind, bool begin);
     bool launch_ahead(uint64_t root, uint64_t step, bool with_grads);
+    const uint64_t* captured_seed(uint64_t root, uint64_t step, cudaStream_t s);
 
     Context* ctx_;
     int method_;
@@ -187,6 +190,8 @@ class Plan {
     // overlapped power iteration (decompose): Gram + Cholesky-inverse on side_ next to the product X Y
     bool overlap_orth_ = false;  // opt-in (RKFAC_OVERLAP_ORTH=1): see decompose()
     int explicit_tail_ = 1;  // trailing products kept in the reference's order
+    uint64_t* h_seed_ = nullptr;  // pinned (root, step) read by captured steps at replay
+    DevBuf d_seed_;
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_pre_ = nullptr, ev_copy_ = nullptr;
     bool step_overlap_ = false;  // step(): Omega / gradient copy next to the EA update, U^T copy-out next to the apply

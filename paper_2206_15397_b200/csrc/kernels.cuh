@@ -20,7 +20,7 @@ struct OmegaDesc {
 };
 // mode 0: seed_f = desc.seed; mode 1: seed_f = substream(root, step, tag_f)
 void launch_omega(const OmegaDesc* d_descs, int nfactors, long long total, int mode, uint64_t root, uint64_t step,
-                  cudaStream_t s);
+                  cudaStream_t s, const uint64_t* seed_src = nullptr);
 
 struct CholDesc {
     int w;

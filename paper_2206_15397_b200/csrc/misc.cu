@@ -25,7 +25,11 @@ __device__ __forceinline__ int find_desc(const OmegaDesc* descs, int n, long lon
 // K1: rng.hpp:59-63 sample_gaussian, every factor in one launch; FP64 transcendental math, FP32 store.
 // Threads walk Omega^T (w x d) in storage order: consecutive threads -> consecutive i -> coalesced stores.
 __global__ void omega_kernel(const OmegaDesc* __restrict__ descs, int n, long long total, int mode, uint64_t root,
-                             uint64_t step) {
+                             uint64_t step, const uint64_t* __restrict__ seed_src) {
+    if (seed_src) {  // a captured step: (root, step) are read at replay time (rkfac_plan_set_step_seed)
+        root = seed_src[0];
+        step = seed_src[1];
+    }
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int f = find_desc(descs, n, e);
@@ -141,10 +145,10 @@ __global__ void transpose_kernel(const float* __restrict__ in, long long ldi, in
 }  // namespace
 
 void launch_omega(const OmegaDesc* d_descs, int nfactors, long long total, int mode, uint64_t root, uint64_t step,
-                  cudaStream_t s) {
+                  cudaStream_t s, const uint64_t* seed_src) {
     if (total == 0) return;
     const int blocks = (int)std::min<long long>(ceil_div(total, 256), kNumSMs * 16);
-    omega_kernel<<<blocks, 256, 0, s>>>(d_descs, nfactors, total, mode, root, step);
+    omega_kernel<<<blocks, 256, 0, s>>>(d_descs, nfactors, total, mode, root, step, seed_src);
     count_launch();
     RKFAC_CHECK_LAUNCH();
 }

@@ -1151,7 +1151,8 @@ void TcGemm::finalize() {
     }();
     // CTA pairs need enough 256-row tiles to fill the SM pairs; an under-filled launch (a multi-GPU shard, a
     // single-factor call) goes back to single-CTA tiles and the N split below (same K order per element: bitwise)
-    if (two_cta_ && (int)tiles_.size() * 2 < pair_slots()) {
+    // (only a launch that owns the GPU: a capped one shares it with the other groups' launches)
+    if (two_cta_ && cap_ == 0 && (int)tiles_.size() * 2 < pair_slots()) {
         two_cta_ = false;
         std::vector<TcProblemDesc> nd = descs_;
         probs_.clear(); maps_.clear(); tiles_.clear(); descs_.clear();
