@@ -34,8 +34,8 @@ OMEGA_ROOT = 7
 GRAD_ROOT = 99
 # dram__bytes_read.sum + dram__bytes_write.sum of one X*Q launch of THIS workload, from that workload's own ncu --set
 # full capture (profiles/); None for a workload not captured yet
-XQ_TRAFFIC = {"vgg16": 626528768 + 20797952}  # X read once; its lo plane is formed in smem
-XQ_TRAFFIC_SRC = {"vgg16": "profiles/r01_xq_full.txt (dram__bytes_read.sum + dram__bytes_write.sum)"}
+XQ_TRAFFIC = {"vgg16": 606247680 + 29901312}  # X read once; its lo plane is formed in smem
+XQ_TRAFFIC_SRC = {"vgg16": "profiles/r02_xq_full.txt (dram__bytes_read.sum + dram__bytes_write.sum; CTA-pair kernel)"}
 
 VGG_A = [28, 577, 577, 1153, 1153, 2305, 2305, 2305, 4609, 4609, 4609, 4609, 4609, 513, 513, 513]
 VGG_G = [64, 64, 128, 128, 256, 256, 256, 512, 512, 512, 512, 512, 512, 512, 512, 10]
@@ -665,7 +665,8 @@ def run_ours(args, wl):
             "stage_ms": stages,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": xq_peak, "unit": "TFLOP/s",
                          "frac": achieved / xq_peak, "traffic": XQ_TRAFFIC.get(args.workload),
-                         "kernel": "tc_gemm_kernel: grouped X*Q product (all factors, one launch), tcgen05 3xTF32",
+                         "kernel": "tc_gemm_kernel<3>: grouped X*Q product (all factors, one launch), tcgen05 3xTF32 on "
+                                   "CTA pairs (cta_group::2); fallback to single-CTA tiles when under-filled",
                          "peak_basis": f"{basis} {'sustained' if capped else 'burst'} bf16 "
                                        f"{peaks.get(peak_key, peaks['bf16_tflops'])} TF/s / 2 (TF32) / 3 (3xTF32 MMAs "
                                        f"per FMA); {'power cap or clock below max' if capped else 'no cap, max clock'}"
