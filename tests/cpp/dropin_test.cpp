@@ -3,6 +3,8 @@
 // sign-invariant reconstruction, eigenvalues and preconditioned gradient are compared (test infrastructure;
 // built by oracle/Makefile into oracle/_ref/dropin_test, run by tests/test_gpu_dropin.py on the GPU box).
 #include <rkfac/kfactor.hpp>
+#include <rkfac/network.hpp>
+#include <rkfac/optimizer.hpp>
 #include <rkfac/rnla.hpp>
 #include <rkfac/rng.hpp>
 
@@ -10,6 +12,7 @@
 #include <cstdio>
 
 #include "rkfac_gpu.hpp"
+#include "rkfac_gpu_optimizer.hpp"
 
 using namespace rkfac;
 
@@ -84,6 +87,53 @@ int main() {
         const bool ok2 = r0.counter == r1.counter && e_p < 1e-4 && b.s.size() == a.s.size();
         fails += ok2 ? 0 : 1;
         std::printf(", \"rsvd\": {\"usv\": %.3e, \"counter_match\": %d}", e_p, int(r0.counter == r1.counter));
+    }
+    // the batched optimizer step (optimizer.hpp:139-222) through the plan: two identical nets, the reference's
+    // optimizer_step on one and rkfac::gpu::optimizer_step on the other, over the T_KI cache schedule
+    // (step 0 decomposes, step 1 reuses, step 2 decomposes again), for SRE-KFAC and RS-KFAC
+    {
+        const std::size_t d_in = 72, n = 96;
+        double worst = 0.0, worst_cache = 0.0;
+        int cache_ok = 1;
+        for (Method method : {Method::SRE_KFAC, Method::RS_KFAC}) {
+            RngState init_a(11), init_b(11);
+            Mlp net_cpu(d_in, {96, 64}, 10, 0.95, init_a), net_gpu(d_in, {96, 64}, 10, 0.95, init_b);
+            for (Mlp* net : {&net_cpu, &net_gpu})
+                for (LayerState& L : net->layers()) {  // zero-init EA (parity fixtures)
+                    L.a_factor = EAKFactor(L.a_factor.dim(), 0.95, true);
+                    L.g_factor = EAKFactor(L.g_factor.dim(), 0.95, true);
+                }
+            OptimizerConfig cfg;
+            cfg.method = method;
+            cfg.n_pwr_it = 2;
+            ResolvedSchedule sch;
+            sch.lambda = 0.1; sch.target_rank = 24; sch.oversampling = 8; sch.t_ki = 2;
+            const RngState rng(4242);
+            for (std::size_t step = 0; step < 3; ++step) {
+                Batch b;
+                RngState g = RngState(77).substream(step, 0);
+                b.x = sample_gaussian(g, d_in, n);
+                for (std::size_t i = 0; i < d_in; ++i)
+                    for (std::size_t c = 0; c < n; ++c) b.x(i, c) /= double(i + 1);
+                for (std::size_t c = 0; c < n; ++c) b.y.push_back(int(g.next_u64() % 10));
+                const ForwardResult fw = net_cpu.forward(b);
+                const BackwardResult bw = net_cpu.backward(b);
+                net_cpu.accumulate_factors(fw.a_matrices, bw.g_matrices);
+                gpu::accumulate_factors(net_gpu, fw.a_matrices, bw.g_matrices);
+                const StepResult ra = optimizer_step(net_cpu, bw.gradients, cfg, sch, step, rng);
+                const StepResult rb = gpu::optimizer_step(net_gpu, bw.gradients, cfg, sch, step, rng);
+                for (std::size_t l = 0; l < ra.updates.size(); ++l) worst = std::max(worst, rel(rb.updates[l], ra.updates[l]));
+                for (std::size_t l = 0; l < net_cpu.n_layers(); ++l) {  // the mirrored caches follow the reference's
+                    const LowRankEig &ca = *net_cpu.layers()[l].cached_a_decomp, &cb = *net_gpu.layers()[l].cached_a_decomp;
+                    cache_ok &= int(ca.method == cb.method && ca.rank() == cb.rank());
+                    worst_cache = std::max(worst_cache, rel(lowrank_reconstruct(cb), lowrank_reconstruct(ca)));
+                }
+            }
+        }
+        const bool ok = worst < 1e-4 && worst_cache < 1e-4 && cache_ok;
+        fails += ok ? 0 : 1;
+        std::printf(", \"optimizer_step\": {\"updates\": %.3e, \"cached_recon\": %.3e, \"cache_ok\": %d}", worst,
+                    worst_cache, cache_ok);
     }
     // error behaviour mirrors the reference exceptions
     bool threw = false;

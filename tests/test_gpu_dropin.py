@@ -19,3 +19,7 @@ def test_cpp_dropin_matches_reference():
     for m in ("srevd", "rsvd_psd"):
         assert res[m]["counter_match"] == 1
         assert res[m]["recon"] < 1e-4 and res[m]["eig"] < 1e-4 and res[m]["precond"] < 1e-4
+    # the batched optimizer step (include/rkfac_gpu_optimizer.hpp) vs rkfac::optimizer_step on an identical net over
+    # the T_KI cache schedule, SRE-KFAC and RS-KFAC: updates and the mirrored cached decompositions
+    opt = res["optimizer_step"]
+    assert opt["cache_ok"] == 1 and opt["updates"] < 1e-4 and opt["cached_recon"] < 1e-4
