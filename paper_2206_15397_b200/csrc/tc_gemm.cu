@@ -1094,7 +1094,13 @@ int TcGemm::add(const TcProblemDesc& d) {
         if (kb0 >= kb1) continue;
         // tall problems (>= 8 row tiles, unsplit, not symmetric): pairs of row tiles share each B tile (halves the
         // L2->SM traffic of B, the re-read operand); the accumulation order per element is unchanged (bitwise)
-        const bool pairs = !d.sym && ks == 1 && ntm >= 8 && !two_cta_;
+        // (long K only: a pair occupies both TMEM accumulators, so its epilogue cannot overlap the next tile's
+        // mainloop -- for short-K products such as Y L^-T (K = w) that serialisation costs more than the B re-read)
+        static const int pair_min_kb = [] {
+            const char* e = std::getenv("RKFAC_TC_PAIR_MIN_KB");
+            return e ? std::atoi(e) : 48;
+        }();
+        const bool pairs = !d.sym && ks == 1 && ntm >= 8 && !two_cta_ && (kb1 - kb0) >= pair_min_kb;
         // units of 128 rows per tile: single CTA 1 (2 when paired); CTA pairs 2
         const int unit = two_cta_ ? 2 : 1;
         for (int tn = 0; tn < ntn; ++tn)
