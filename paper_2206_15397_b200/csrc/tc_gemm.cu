@@ -738,15 +738,17 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
             const bool diag = pr.sym && m0s == tl.n0;
             const int nlim = min(pr.N, tl.n0 + pr.n_tile);
             float (*tile)[kTP] = stage_tiles[warp - 2];
-            // prefetch the first Cin chunk (row-major axpy input, e.g. the EA factor) before the accumulator is ready
-            const bool pf = kCfg != 2 && pr.beta != 0.f && pr.cin_t == 0 && pr.ksplit <= 1;
-            float4 pre[8];
-            if (pf) rm_issue(pre, pr.Cin, pr.ldcin, mbase, tl.n0, pr.M, nlim, lane);
+            // (an axpy input Cin outside the EA configuration -- kCfg 2 prefetches it through its cp.async ring -- is
+            // loaded chunk by chunk: no problem on the path takes that route, and a register-held prefetch costs the
+            // 32 registers that keep this epilogue from spilling)
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kMaxBN;
+            // kCfg 0/1/3: the next chunk's TMEM load is issued as soon as this chunk's accumulators are consumed, so
+            // its latency overlaps this chunk's epilogue (short-K products are epilogue-bound)
+            uint32_t r[32];
+            if constexpr (kCfg != 2) tmem_ld32_issue(tbase, r);
             for (int c0 = 0; c0 < pr.n_tile; c0 += 32) {
-                uint32_t r[32];
                 if constexpr (kCfg == 2) {
                     // the TMEM load in flight while this chunk's Cin cp.async group is awaited (every EA tile has a
                     // Cin, host-checked: chunk_no's slot is complete once at most one younger group is pending)
@@ -754,7 +756,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                     asm volatile("cp.async.wait_group %0;\n" ::"n"(kCinRing - 2) : "memory");
                     tmem_ld32_wait(r);
                 } else {
-                    tmem_ld32(tbase + c0, r);
+                    tmem_ld32_wait(r);
                 }
                 const int nbase = tl.n0 + c0;
                 if (pr.ksplit > 1) {  // raw partials, column-major per slice: each store is 128 B across the warp
@@ -764,11 +766,15 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                         for (int j = 0; j < 32; ++j)
                             if (nbase + j < nlim) part[(long long)j * pr.M] = __uint_as_float(r[j]);
                     }
+                    if constexpr (kCfg != 2)
+                        if (c0 + 32 < pr.n_tile) tmem_ld32_issue(tbase + c0 + 32, r);
                     continue;
                 }
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = pr.alpha * __uint_as_float(r[j]);
+                if constexpr (kCfg != 2)
+                    if (c0 + 32 < pr.n_tile) tmem_ld32_issue(tbase + c0 + 32, r);
                 if (pr.rs) {
                     const float sr = (m < pr.M) ? pr.rs[m] : 0.f;
 #pragma unroll
@@ -830,12 +836,7 @@ tc_gemm_kernel(const TcProb* __restrict__ probs, const CUtensorMap* __restrict__
                 }
                 if (pr.beta != 0.f) {
                     float cv[32];
-                    if (pf) {
-                        rm_finish(cv, pre, tile, lane);
-                        if (c0 + 32 < pr.n_tile) rm_issue(pre, pr.Cin, pr.ldcin, mbase, nbase + 32, pr.M, nlim, lane);
-                    } else {
-                        chunk_load(cv, pr.Cin, pr.ldcin, pr.cin_t, mbase, nbase, pr.M, nlim, tile, lane);
-                    }
+                    chunk_load(cv, pr.Cin, pr.ldcin, pr.cin_t, mbase, nbase, pr.M, nlim, tile, lane);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = fmaf(pr.beta, cv[j], v[j]);
                 }
