@@ -460,6 +460,9 @@ def run_ours(args, wl):
         for dst, src in ((step.samples, probe.samples), (step.grads, probe.grads)):
             for a, b in zip(dst, src):
                 a.copy_(b)
+    if args.overlap:
+        step.set_overlap(True)
+        probe.set_overlap(True)
     torch.cuda.synchronize()
 
     send = torch.zeros(layout.chunk, dtype=torch.float32, device=dev)
@@ -656,7 +659,7 @@ def run_ours(args, wl):
                        "oversampling": p, "power_iters": q, "lambda": lam, "n": n, "method": "srevd",
                        "parallelism": f"layer-LPT x{world}" + (" + NCCL all-gather" if world > 1 else " (no collective on one GPU)"),
                        "streams_per_gpu": args.groups,
-                       "cuda_graph": bool(args.graph),
+                       "cuda_graph": bool(args.graph), "overlapped_power_iteration": bool(args.overlap),
                        "l2": f"inputs ({sum(4 * d * d for a, g in layers for d in (a, g)) / 1e6:.0f} MB of factors) "
                              "exceed the 126 MB L2; no flush",
                        "value_def": "factors inverted per second of the whole step (EA + rand-EVD + precondition "
@@ -704,6 +707,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=5, help="layer groups on concurrent streams (StreamedStep; 5 gave the best e2e)")
     ap.add_argument("--profile-step", action="store_true", help="run one step under cudaProfilerStart/Stop and exit")
+    ap.add_argument("--overlap", action="store_true",
+                    help="opt-in overlapped power iteration (rkfac_plan_set_overlap; shortens a shard's latency chain, "
+                         "parity holds while lambda_r / lambda_1 >~ 1e-5: DESIGN.md 4.1)")
     ap.add_argument("--trace", default="", help="write the kernel timeline of one step (chrome trace) and exit")
     ap.add_argument("--emulate-world", type=int, default=0, help="run one shard of an N-GPU job alone (projection)")
     ap.add_argument("--emulate-rank", type=int, default=0)

@@ -207,6 +207,14 @@ int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
  * the reference draws a fresh substream per step), so one graph serves every step id. */
 int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambda);
 int rkfac_plan_set_step_seed(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
+/* Overlapped power iteration (off by default): the middle products of randomized_range (rnla.hpp:47-56) are formed
+ * as Y' = (X Y) L^-T, L = chol(Y^T Y), so the product runs next to the Gram + Cholesky-inverse instead of after them
+ * (same iterate in exact arithmetic; the last product keeps the reference's order).  It shortens the per-factor
+ * latency chain (a lone 4609-wide layer: 4.7 -> 3.7 ms), but the rounding of the Gram coefficients reaches the last
+ * Ritz values as ~(6e-8 * lambda_1 / lambda_r)^2: within the 1e-4 bar while lambda_r / lambda_1 >~ 1e-5 (configs
+ * 1-3 pass their parity tests with it), beyond it below that (config 5: 3e-4).  Enable it for factors whose retained
+ * spectrum spans less than five decades. */
+int rkfac_plan_set_overlap(rkfac_plan_t plan, int enabled);
 /* Cap the persistent tensor-core grids of this plan at `ctas` CTAs (0: one per SM), leaving SMs to the
  * latency-bound per-factor kernels of plans running concurrently on other streams (StreamedStep). */
 int rkfac_plan_set_max_ctas(rkfac_plan_t plan, int ctas);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "rkfac_plan_decompose": (C.c_int, [_vp, _c_u64, _c_u64]),
     "rkfac_plan_ea_decompose": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64]),
     "rkfac_plan_set_step_seed": (C.c_int, [_vp, _c_u64, _c_u64]),
+    "rkfac_plan_set_overlap": (C.c_int, [_vp, C.c_int]),
     "rkfac_plan_precondition": (C.c_int, [_vp, C.c_double]),
     "rkfac_plan_step": (C.c_int, [_vp, C.c_double, C.c_double, _c_u64, _c_u64, C.c_double]),
     "rkfac_plan_timing": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
@@ -586,6 +587,11 @@ class BatchedStep:
         _check(self.ctx.lib.rkfac_plan_step(self.h, rho, scale, _c_u64(rng_root), _c_u64(step), lam), self.ctx.h,
                "plan_step")
 
+    def set_overlap(self, on: bool):
+        """Overlapped power iteration (rkfac_plan_set_overlap; off by default): shorter per-factor latency chain,
+        tail Ritz values perturbed by ~(6e-8 lambda_1 / lambda_r)^2 -- see :func:`overlap_error_estimate`."""
+        _check(self.ctx.lib.rkfac_plan_set_overlap(self.h, 1 if on else 0), self.ctx.h, "plan_set_overlap")
+
     def set_step_seed(self, rng_root: int, step: int):
         """(rng_root, step) of the next replay of a CUDA graph captured from this plan's step / decomposition."""
         _check(self.ctx.lib.rkfac_plan_set_step_seed(self.h, _c_u64(rng_root), _c_u64(step)), self.ctx.h,
@@ -639,6 +645,17 @@ class BatchedStep:
 
 
 STREAMED_TC_CTAS = 132
+
+
+def overlap_error_estimate(dvals) -> float:
+    """Predicted relative perturbation of the last retained Ritz value under the overlapped power iteration
+    (``set_overlap``): (2^-24 * lambda_1 / lambda_r)^2, from the eigenvalues of a previous decomposition of the factor
+    (K-FAC spectra move slowly between T_KI refreshes).  Enable the overlap while this stays below the parity bar."""
+    d = dvals.detach().double().cpu() if hasattr(dvals, "detach") else dvals
+    top, last = float(d[0]), float(d[len(d) - 1])
+    if last <= 0.0:
+        return float("inf")
+    return (2.0 ** -24 * top / last) ** 2
 
 
 class StepGraph:
@@ -816,6 +833,10 @@ class StreamedStep:
     def set_step_seed(self, rng_root: int, step: int):
         for sub in self.subs:
             sub.set_step_seed(rng_root, step)
+
+    def set_overlap(self, on: bool):
+        for sub in self.subs:
+            sub.set_overlap(on)
 
     def step_host(self, rng_root: int, step: int, lam: float, h_samples, h_grads, h_outs, rho: float = 0.95,
                   scale: float = 1.0, timeline: Optional[list] = None):

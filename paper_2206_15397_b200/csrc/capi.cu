@@ -388,6 +388,10 @@ int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambd
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->prepare(rho, scale, lambda); });
 }
 
+int rkfac_plan_set_overlap(rkfac_plan_t plan, int enabled) {
+    return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_overlap(enabled != 0); });
+}
+
 int rkfac_plan_set_step_seed(rkfac_plan_t plan, uint64_t root, uint64_t step) {
     return guarded(plan ? plan->ctx : nullptr, [&] { plan->p->set_step_seed(root, step); });
 }

@@ -105,6 +105,8 @@ class Plan {
     // EA operands' TF32 lo planes: -1 automatic (stored by a split pass when n >= 512), 0 formed in shared memory,
     // 1 stored by a split pass (arithmetic identical; rkfac_plan_set_ea_lo_mode)
     void set_ea_lo_mode(int mode);
+    // overlapped power iteration (see decompose()): off by default
+    void set_overlap(bool on) { overlap_orth_ = on; }
 
     void ea_update(double rho, double scale);
     // mode 1: seeds from substream(root, step, tag); mode 0: explicit seeds.

@@ -33,18 +33,20 @@ def main():
     ap.add_argument("--worlds", default="2,4,8")
     ap.add_argument("--busbw-gbs", type=float, default=700.0, help="assumed all-gather bus bandwidth (not measured)")
     ap.add_argument("--workload", default="vgg16")
+    ap.add_argument("--overlap", action="store_true", help="shards with the opt-in overlapped power iteration")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     if args.out is None:
-        sfx = "" if args.workload == "vgg16" else "_" + args.workload
+        sfx = ("" if args.workload == "vgg16" else "_" + args.workload) + ("_overlap" if args.overlap else "")
         args.out = os.path.join(ROOT, "profiles", f"r02_shard_projection{sfx}.json")
     import bench
     from paper_2206_15397_b200.partition import layer_cost, lpt_partition
 
     layers, _, _, r, p = bench.WORKLOADS[args.workload][:5]
-    one = run([], args.steps, args.workload)
+    ov = ["--overlap"] if args.overlap else []
+    one = run(ov, args.steps, args.workload)
     t1 = one["ms_per_step"]
-    res = {"workload": args.workload, "t1_ms": t1, "t1_line": {k: one[k] for k in ("ms_per_step", "stage_ms", "clocks")}, "worlds": {}}
+    res = {"workload": args.workload, "overlapped_power_iteration": bool(args.overlap), "t1_ms": t1, "t1_line": {k: one[k] for k in ("ms_per_step", "stage_ms", "clocks")}, "worlds": {}}
     costs = [layer_cost(a, g, r, p) for a, g in layers]
     for N in (int(x) for x in args.worlds.split(",")):
         parts = lpt_partition(costs, N)
@@ -53,7 +55,7 @@ def main():
             if not parts[k]:
                 shards.append({"rank": k, "layers": [], "ms": 0.0})
                 continue
-            ln = run(["--emulate-world", str(N), "--emulate-rank", str(k)], args.steps, args.workload)
+            ln = run(["--emulate-world", str(N), "--emulate-rank", str(k)] + ov, args.steps, args.workload)
             shards.append({"rank": k, "layers": parts[k], "ms": ln["ms_per_step"], "stage_ms": ln["stage_ms"]})
             print(f"N={N} rank {k} layers {parts[k]}: {ln['ms_per_step']:.3f} ms", flush=True)
         tmax = max(s["ms"] for s in shards)
