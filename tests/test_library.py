@@ -84,3 +84,15 @@ def test_cpp_dropin_compiles_against_reference_headers():
     out = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", ref_inc, "-I", os.path.join(ROOT, "include"),
                           "-I", "/usr/local/cuda/include", src], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr[-2000:]
+
+
+def test_c_abi_header_is_plain_c(tmp_path):
+    """include/rkfac_b200.h is the FFI boundary: it must compile as C99 (cgo / JNI / ctypes-style hosts), with no
+    C++ or torch types in any signature."""
+    src = tmp_path / "hdr.c"
+    src.write_text('#include "rkfac_b200.h"\nint main(void) { rkfac_factor_desc d; d.dim = 1; return (int)d.dim - 1; }\n')
+    out = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only", "-I",
+                          os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr[-2000:]
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    assert "torch" not in text and "std::" not in text and "at::" not in text
