@@ -204,7 +204,9 @@ int rkfac_plan_set_timing(rkfac_plan_t plan, int enabled);
 /* Build every stage rkfac_plan_step(rho, scale, *, *, lambda) uses without launching anything, so the step only
  * enqueues kernels and may be captured into a CUDA graph.  A captured step reads (rng_root, step) from a pinned host
  * pair at every replay: rkfac_plan_set_step_seed before the replay gives that replay its Omega (optimizer.hpp:189:
- * the reference draws a fresh substream per step), so one graph serves every step id. */
+ * the reference draws a fresh substream per step), so one graph serves every step id.  The pair is read by a copy
+ * node of the replay, asynchronously: write a new pair only after the previous replay has consumed the old one (e.g.
+ * after an event recorded behind that replay). */
 int rkfac_plan_prepare(rkfac_plan_t plan, double rho, double scale, double lambda);
 int rkfac_plan_set_step_seed(rkfac_plan_t plan, uint64_t rng_root, uint64_t step);
 /* Overlapped power iteration (off by default): the middle products of randomized_range (rnla.hpp:47-56) are formed

@@ -658,6 +658,23 @@ def overlap_error_estimate(dvals) -> float:
     return (2.0 ** -24 * top / last) ** 2
 
 
+def _replay_with_seed(g, rng_root, step):
+    """The pinned (root, step) pair is read by a copy node of the replay, asynchronously: a NEW pair may only be
+    written once the previous replay has consumed the old one, so a change of seed first waits for the event recorded
+    behind the previous replay (free when, as in training, other work separates two K-FAC steps)."""
+    torch = _torch()
+    if rng_root is not None and (rng_root, step) != getattr(g, "_seed", None):
+        ev = getattr(g, "_last", None)
+        if ev is not None:
+            ev.synchronize()
+        g.step_obj.set_step_seed(rng_root, step)
+        g._seed = (rng_root, step)
+    g.graph.replay()
+    if getattr(g, "_last", None) is None:
+        g._last = torch.cuda.Event()
+    g._last.record(torch.cuda.current_stream(g.step_obj.device))
+
+
 class StepGraph:
     """One full preconditioned step (EA -> rand-EVD -> precondition of every layer, every group's stream) captured
     once as a CUDA graph and replayed: ~70 dependent launches per group chain are submitted as one graph launch, so the
@@ -686,9 +703,7 @@ class StepGraph:
     def replay(self, rng_root: Optional[int] = None, step: Optional[int] = None):
         """Replay the captured step; (rng_root, step), when given, select this replay's Omega substreams (the captured
         step reads them from a pinned host pair: rkfac_plan_set_step_seed), else the pair of the last replay."""
-        if rng_root is not None:
-            self.step_obj.set_step_seed(rng_root, step)
-        self.graph.replay()
+        _replay_with_seed(self, rng_root, step)
 
 
 class HostStepGraph:
@@ -717,9 +732,7 @@ class HostStepGraph:
         self.launches = step_obj.ctx.launches() - n0
 
     def replay(self, rng_root: Optional[int] = None, step: Optional[int] = None):
-        if rng_root is not None:
-            self.step_obj.set_step_seed(rng_root, step)
-        self.graph.replay()
+        _replay_with_seed(self, rng_root, step)
 
 
 class StreamedStep:
