@@ -238,3 +238,22 @@ def test_config5_size_exact_low_rank_recovery_and_eq11_identity(cuda):
     out = rk.apply_lowrank_damped_inverse(lr, lam, top, rk.ApplySide.LEFT)
     expect = top.double() / (dv[:16][None, :] + lam)
     assert float(torch.linalg.norm(out.double() - expect) / torch.linalg.norm(expect)) < TOL  # measured 1.4e-5
+
+
+def test_cta_pair_kernel_is_bitwise_the_single_cta_kernels_on_unaligned_shapes():
+    """The X*Q products on CTA pairs (tcgen05 cta_group::2) keep every element's K order: a step over 32 factors whose
+    dimensions sit off every tile boundary hashes identically with RKFAC_XQ_PAIR=1 and =0 (the switch is read once per
+    process, hence the two subprocesses; tools/pair_bitwise.py)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for pair in ("1", "0"):
+        env = dict(os.environ, RKFAC_XQ_PAIR=pair)
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "pair_bitwise.py"), "2", "1", "mixed"],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout.strip().splitlines())
+    assert len(outs[0]) == 2 and outs[0] == outs[1]

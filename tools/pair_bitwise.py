@@ -2,7 +2,8 @@
 """Stress check of the CTA-pair X*Q kernel: the VGG16 step's outputs hashed over repeated steps.  Run once with
 RKFAC_XQ_PAIR=1 and once with RKFAC_XQ_PAIR=0 (the single-CTA kernels): every hash must agree -- the pair kernel
 keeps each element's K order, so any difference is a synchronisation bug (a stale operand read).
-usage: python tools/pair_bitwise.py [reps] -> one line per repetition: sha256 of all U^T, eigenvalues and outputs"""
+usage: python tools/pair_bitwise.py [reps] [groups] [vgg16|mixed] -> one line per repetition: sha256 of all U^T,
+eigenvalues and outputs ("mixed": many mid-size factors with dimensions off every tile boundary, rank 96)"""
 import hashlib
 import math
 import os
@@ -19,7 +20,13 @@ import paper_2206_15397_b200 as rk  # noqa: E402
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     groups = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-    layers, n, e, r, p, q, lam, _ = bench.WORKLOADS["vgg16"]
+    which = sys.argv[3] if len(sys.argv) > 3 else "vgg16"
+    if which == "mixed":  # enough 256-row tiles to stay on the pair kernel, none of them aligned
+        dims = [130, 257, 300, 511, 640, 1000, 1153, 1290, 1535, 2049, 2305, 777, 897, 1025, 385, 129]
+        layers = [(dims[i], dims[(i + 5) % len(dims)]) for i in range(len(dims))]
+        n, e, r, p, q, lam = 96, 1.0, 96, 10, 2, 0.1
+    else:
+        layers, n, e, r, p, q, lam, _ = bench.WORKLOADS["vgg16"]
     dev = torch.device("cuda", 0)
     specs = [rk.LayerSpec(a, g) for a, g in layers]
     if groups > 1:
