@@ -84,7 +84,7 @@ def load_peaks():
 
 # ------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    def __init__(self, device_index=0, period=0.1):
+    def __init__(self, device_index=0, period=0.02):  # the timed region is ~0.1 s: several samples under load
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period = period
         self.dev = device_index
