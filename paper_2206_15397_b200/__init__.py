@@ -762,7 +762,10 @@ class StreamedStep:
         if max_ctas is None:
             # a persistent tensor-core grid on every SM would keep the other groups' latency-bound kernels (Cholesky-
             # inverse, tridiagonalisation clusters) waiting; 132 of 148 measured best for 2 VGG16 groups
-            max_ctas = STREAMED_TC_CTAS if len(self.parts) > 1 else 0
+            # (with more groups each grid gets a smaller share: 2 x 148 / groups, between 64 and 132 -- measured with
+            # 5 VGG16 groups: 148 / 132 / 100 / 64 / 48 CTAs -> 7.02 / 7.01 / 6.96 / 6.93 / 6.95 ms)
+            g = len(self.parts)
+            max_ctas = max(64, min(STREAMED_TC_CTAS, (2 * 148 // g) & ~1)) if g > 1 else 0
         ns = list(n_samples)
         self.subs = []
         for part in self.parts:
